@@ -1,0 +1,111 @@
+/* geodist_b200 — C-ABI boundary of the B200-native generalised geodesic
+ * distance transform (arXiv 2208.00001 / FastGeodis raster scan).
+ *
+ * Plain pointers and sizes only.  Every entry point validates on the host
+ * first (same conditions as the reference, which throws before computing) and
+ * returns a status code; gd_last_error() gives the message for the calling
+ * thread.  Grids follow the reference's ScalarGrid convention
+ * (/root/reference/proj/include/geodist/grid.hpp:15-74): `ndim` 2 or 3,
+ * logical dims/spacing in (depth,) height, width order, row-major with width
+ * fastest.  Batched calls take `batch` such grids back to back.
+ *
+ * Memory: `mem` = GD_MEM_HOST (pointers are host memory; the library stages
+ * through the device and synchronises before returning, like the reference's
+ * blocking calls) or GD_MEM_DEVICE (pointers are device memory on the current
+ * CUDA device; work is enqueued on `stream` (a cudaStream_t, NULL = legacy
+ * default stream).  Calls that must read a device-side result to decide
+ * control flow — the mask-range / image-exactness check, GSF's empty-complement
+ * test, fixpoint convergence — synchronise `stream`).
+ *
+ * There is no CPU fallback: if no CUDA device is usable every call returns
+ * GD_CUDA_ERROR.
+ */
+#ifndef GEODIST_B200_H
+#define GEODIST_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GD_VERSION 1
+
+enum gd_status {
+    GD_OK = 0,
+    GD_INVALID_ARGUMENT = 1, /* reference: std::invalid_argument */
+    GD_EMPTY_SEEDS = 2,      /* reference: geodist::EmptySeedsError (transforms.hpp:11-14) */
+    GD_CUDA_ERROR = 3,       /* device failure; C++ layer throws std::runtime_error */
+    GD_UNSUPPORTED = 4       /* shape beyond the kernels' co-residency limit */
+};
+
+enum gd_mem { GD_MEM_HOST = 0, GD_MEM_DEVICE = 1 };
+
+typedef struct gd_grid {
+    int ndim;          /* 2 or 3 */
+    int dims[3];       /* first ndim entries used: (depth,) height, width */
+    double spacing[3]; /* same order; finite and > 0 */
+} gd_grid;
+
+typedef struct gd_stats {
+    int rounds;            /* TransformStats::rounds (transforms.hpp:33-37) */
+    int converged;         /* TransformStats::converged */
+    int complement_empty;  /* TransformStats::complement_empty */
+    double last_change;    /* FixpointResult::last_change (scan_parallel.hpp:31-36) */
+    long long kernel_launches;
+} gd_stats;
+
+/* generalized_geodesic — replaces geodist::generalized_geodesic
+ * (/root/reference/proj/include/geodist/transforms.hpp:62-64, src/transforms.cpp:143-158):
+ * out = scan(image, min(nu * soft_mask, 1e10)) with `iterations` rounds of the
+ * directional passes.  `stats` may be NULL. */
+int gd_generalized_geodesic(const gd_grid* grid, const float* image, const float* soft_mask,
+                            double lambda, double nu, int iterations, float* out, int mem,
+                            void* stream, gd_stats* stats);
+
+/* Batched generalized_geodesic over `batch` independent grids of identical
+ * shape (new: the reference has no batch entry; a loop over
+ * generalized_geodesic is its equivalent). */
+int gd_generalized_geodesic_batched(const gd_grid* grid, int batch, const float* images,
+                                    const float* soft_masks, double lambda, double nu,
+                                    int iterations, float* out, int mem, void* stream,
+                                    gd_stats* stats);
+
+/* gsf — replaces geodist::gsf (transforms.hpp:85-86, transforms.cpp:231-238):
+ * geodesic_erode(geodesic_dilate(M, theta), theta); binary {0,1} output. */
+int gd_gsf(const gd_grid* grid, const float* image, const float* soft_mask, double lambda,
+           double nu, int iterations, double theta, float* out, int mem, void* stream,
+           gd_stats* stats);
+
+/* directional_pass — replaces geodist::directional_pass /
+ * detail::directional_pass_inplace (scan_parallel.hpp:20-22,45-47): one pass
+ * along canonical axis (0 depth, 1 height, 2 width) and orientation +-1,
+ * relaxing `dist` in place. */
+int gd_directional_pass(const gd_grid* grid, const float* image, float* dist, int axis,
+                        int orientation, double lambda, int mem, void* stream);
+
+/* parallel_scan — replaces geodist::parallel_scan / detail::parallel_scan_inplace
+ * (scan_parallel.hpp:27-28,48-50): `iterations` rounds of pass_sequence(ndim),
+ * in place on `dist`. */
+int gd_parallel_scan(const gd_grid* grid, const float* image, float* dist, double lambda,
+                     int iterations, int mem, void* stream);
+
+/* scan_to_fixpoint with Engine::Parallel — replaces geodist::scan_to_fixpoint
+ * (scan_parallel.hpp:40-43, scan_parallel.cpp:357-397), in place on `dist`. */
+int gd_scan_to_fixpoint(const gd_grid* grid, const float* image, float* dist, double lambda,
+                        int max_rounds, double tol, int mem, void* stream, gd_stats* stats);
+
+/* Blend (0 < lambda < 1) arithmetic: 0 = f32 (default; within 1e-6 abs +
+ * 1e-5 rel of the reference), 1 = f64 replica of the reference (bit-exact). */
+int gd_set_exact_blend(int on);
+
+/* Utilities. */
+const char* gd_last_error(void);
+int gd_version(void);
+long long gd_kernel_launches(void);
+/* Device-side SplitMix64 benchmark image (tools/main.cpp:67-81). */
+int gd_fill_splitmix(float* device_out, long long n, unsigned long long seed, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GEODIST_B200_H */

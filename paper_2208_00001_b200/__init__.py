@@ -1,0 +1,279 @@
+"""geodist_b200 — B200-native generalised geodesic distance transform.
+
+Python host mirror of the reference's operator interface
+(/root/reference/proj/include/geodist/{transforms,scan_parallel}.hpp) over the
+C-ABI in ``include/geodist_b200.h``.  Every call runs the sm_100a kernels in
+``lib/libgeodist_b200.so``; there is no CPU fallback — importing without the
+built library, or calling without a CUDA device, raises.
+
+Host (numpy) calls mirror ``geodist::*`` one-to-one (same argument meaning and
+error types: ``InvalidArgument`` for the reference's std::invalid_argument,
+``EmptySeedsError`` for geodist::EmptySeedsError).  ``device`` holds the same
+calls on CUDA tensors (torch) enqueued on the current stream.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+__all__ = [
+    "GeodistError", "InvalidArgument", "EmptySeedsError", "UnsupportedShape", "CudaError",
+    "generalized_geodesic", "generalized_geodesic_batched", "gsf", "directional_pass",
+    "parallel_scan", "scan_to_fixpoint", "generalised_geodesic2d", "generalised_geodesic3d",
+    "GSF2d", "GSF3d", "set_exact_blend", "kernel_launches", "device", "LIB_PATH",
+]
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libgeodist_b200.so")
+
+GD_OK, GD_INVALID_ARGUMENT, GD_EMPTY_SEEDS, GD_CUDA_ERROR, GD_UNSUPPORTED = range(5)
+GD_MEM_HOST, GD_MEM_DEVICE = 0, 1
+
+
+class GeodistError(RuntimeError):
+    pass
+
+
+class InvalidArgument(GeodistError, ValueError):
+    pass
+
+
+class EmptySeedsError(GeodistError):
+    pass
+
+
+class CudaError(GeodistError):
+    pass
+
+
+class UnsupportedShape(GeodistError):
+    pass
+
+
+class gd_grid(C.Structure):
+    _fields_ = [("ndim", C.c_int), ("dims", C.c_int * 3), ("spacing", C.c_double * 3)]
+
+
+class gd_stats(C.Structure):
+    _fields_ = [("rounds", C.c_int), ("converged", C.c_int), ("complement_empty", C.c_int),
+                ("last_change", C.c_double), ("kernel_launches", C.c_longlong)]
+
+
+_lib = None
+
+
+def lib():
+    """The loaded C-ABI library (loaded once; raises if it was never built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run __graft_entry__.build() (make -C "
+                              f"paper_2208_00001_b200); there is no CPU fallback")
+        L = C.CDLL(LIB_PATH)
+        vp, d, i, fp = C.c_void_p, C.c_double, C.c_int, C.c_void_p
+        gp, sp = C.POINTER(gd_grid), C.POINTER(gd_stats)
+        L.gd_generalized_geodesic.argtypes = [gp, fp, fp, d, d, i, fp, i, vp, sp]
+        L.gd_generalized_geodesic_batched.argtypes = [gp, i, fp, fp, d, d, i, fp, i, vp, sp]
+        L.gd_gsf.argtypes = [gp, fp, fp, d, d, i, d, fp, i, vp, sp]
+        L.gd_directional_pass.argtypes = [gp, fp, fp, i, i, d, i, vp]
+        L.gd_parallel_scan.argtypes = [gp, fp, fp, d, i, i, vp]
+        L.gd_scan_to_fixpoint.argtypes = [gp, fp, fp, d, i, d, i, vp, sp]
+        L.gd_set_exact_blend.argtypes = [i]
+        L.gd_last_error.restype = C.c_char_p
+        L.gd_kernel_launches.restype = C.c_longlong
+        L.gd_fill_splitmix.argtypes = [fp, C.c_longlong, C.c_ulonglong, vp]
+        _lib = L
+    return _lib
+
+
+def _check(rc: int):
+    if rc == GD_OK:
+        return
+    msg = lib().gd_last_error().decode()
+    if rc == GD_INVALID_ARGUMENT:
+        raise InvalidArgument(msg)
+    if rc == GD_EMPTY_SEEDS:
+        raise EmptySeedsError(msg)
+    if rc == GD_UNSUPPORTED:
+        raise UnsupportedShape(msg)
+    raise CudaError(msg)
+
+
+def _grid(shape, spacing) -> gd_grid:
+    ndim = len(shape)
+    if spacing is None:
+        spacing = (1.0,) * ndim
+    if len(spacing) != ndim:
+        raise InvalidArgument(f"expected {ndim} spacings, got {len(spacing)}")
+    g = gd_grid()
+    g.ndim = ndim
+    for a in range(min(ndim, 3)):
+        g.dims[a] = int(shape[a])
+        g.spacing[a] = float(spacing[a])
+    return g
+
+
+def _f32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def _ptr(a: np.ndarray):
+    return C.c_void_p(a.ctypes.data)
+
+
+def set_exact_blend(on: bool) -> None:
+    """0 < lambda < 1: f64 replica of the reference (bit-exact) instead of f32."""
+    lib().gd_set_exact_blend(1 if on else 0)
+
+
+def kernel_launches() -> int:
+    return int(lib().gd_kernel_launches())
+
+
+# ---------------------------------------------------------------- host API
+def generalized_geodesic(image, soft_mask, spacing=None, lam=1.0, nu=1e10, iterations=2,
+                         stats: dict | None = None) -> np.ndarray:
+    """geodist::generalized_geodesic (transforms.hpp:62-64)."""
+    image, soft_mask = _f32(image), _f32(soft_mask)
+    if image.shape != soft_mask.shape:
+        raise InvalidArgument("generalized_geodesic: shape mismatch")
+    g = _grid(image.shape, spacing)
+    out = np.empty_like(image)
+    st = gd_stats()
+    _check(lib().gd_generalized_geodesic(C.byref(g), _ptr(image), _ptr(soft_mask), lam, nu,
+                                         iterations, _ptr(out), GD_MEM_HOST, None, C.byref(st)))
+    if stats is not None:
+        stats.update(rounds=st.rounds, kernel_launches=st.kernel_launches)
+    return out
+
+
+def generalized_geodesic_batched(images, soft_masks, spacing=None, lam=1.0, nu=1e10,
+                                 iterations=2) -> np.ndarray:
+    """Batch of independent same-shape grids, leading axis = batch."""
+    images, soft_masks = _f32(images), _f32(soft_masks)
+    if images.shape != soft_masks.shape:
+        raise InvalidArgument("shape mismatch")
+    g = _grid(images.shape[1:], spacing)
+    out = np.empty_like(images)
+    _check(lib().gd_generalized_geodesic_batched(C.byref(g), images.shape[0], _ptr(images),
+                                                 _ptr(soft_masks), lam, nu, iterations, _ptr(out),
+                                                 GD_MEM_HOST, None, None))
+    return out
+
+
+def gsf(image, soft_mask, spacing=None, lam=1.0, nu=1e10, iterations=2, theta=0.0):
+    """geodist::gsf (transforms.hpp:85-86).  Returns (mask, rounds, complement_empty)."""
+    image, soft_mask = _f32(image), _f32(soft_mask)
+    if image.shape != soft_mask.shape:
+        raise InvalidArgument("gsf: shape mismatch")
+    g = _grid(image.shape, spacing)
+    out = np.empty_like(image)
+    st = gd_stats()
+    _check(lib().gd_gsf(C.byref(g), _ptr(image), _ptr(soft_mask), lam, nu, iterations, theta,
+                        _ptr(out), GD_MEM_HOST, None, C.byref(st)))
+    return out, st.rounds, bool(st.complement_empty)
+
+
+def directional_pass(dist, image, axis, orientation, spacing=None, lam=1.0) -> np.ndarray:
+    """geodist::directional_pass (scan_parallel.hpp:20-22); returns the new grid."""
+    image = _f32(image)
+    d = _f32(dist).copy()
+    if d.shape != image.shape:
+        raise InvalidArgument("directional_pass: image/distance shape or spacing mismatch")
+    g = _grid(image.shape, spacing)
+    _check(lib().gd_directional_pass(C.byref(g), _ptr(image), _ptr(d), axis, orientation, lam,
+                                     GD_MEM_HOST, None))
+    return d
+
+
+def parallel_scan(image, dist, spacing=None, lam=1.0, iterations=2) -> np.ndarray:
+    """geodist::parallel_scan (scan_parallel.hpp:27-28)."""
+    image = _f32(image)
+    d = _f32(dist).copy()
+    if d.shape != image.shape:
+        raise InvalidArgument("directional_pass: image/distance shape or spacing mismatch")
+    g = _grid(image.shape, spacing)
+    _check(lib().gd_parallel_scan(C.byref(g), _ptr(image), _ptr(d), lam, iterations,
+                                  GD_MEM_HOST, None))
+    return d
+
+
+def scan_to_fixpoint(image, dist, spacing=None, lam=1.0, max_rounds=100, tol=1e-6):
+    """geodist::scan_to_fixpoint, Engine::Parallel.  Returns (dist, rounds, converged, change)."""
+    image = _f32(image)
+    d = _f32(dist).copy()
+    g = _grid(image.shape, spacing)
+    st = gd_stats()
+    _check(lib().gd_scan_to_fixpoint(C.byref(g), _ptr(image), _ptr(d), lam, max_rounds, tol,
+                                     GD_MEM_HOST, None, C.byref(st)))
+    return d, st.rounds, bool(st.converged), st.last_change
+
+
+# Upstream FastGeodis spellings named by the north star.
+def generalised_geodesic2d(image, softmask, v, lamb, iter):  # noqa: A002
+    return generalized_geodesic(image, softmask, None, lamb, v, iter)
+
+
+def generalised_geodesic3d(image, softmask, spacing, v, lamb, iter):  # noqa: A002
+    return generalized_geodesic(image, softmask, spacing, lamb, v, iter)
+
+
+def GSF2d(image, softmask, theta, v, lamb, iter):  # noqa: A002,N802
+    return gsf(image, softmask, None, lamb, v, iter, theta)[0]
+
+
+def GSF3d(image, softmask, theta, spacing, v, lamb, iter):  # noqa: A002,N802
+    return gsf(image, softmask, spacing, lamb, v, iter, theta)[0]
+
+
+# -------------------------------------------------------------- device API
+class device:
+    """Same calls on CUDA tensors (torch), enqueued on the current torch stream."""
+
+    @staticmethod
+    def _stream(stream):
+        if stream is not None:
+            return C.c_void_p(stream)
+        import torch
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    @staticmethod
+    def generalized_geodesic(image, soft_mask, out, spacing=None, lam=1.0, nu=1e10,
+                             iterations=2, batch=None, stream=None):
+        """image/soft_mask/out: contiguous float32 CUDA tensors of shape [B?, (D,) H, W]."""
+        shape = tuple(image.shape)
+        if batch:
+            g = _grid(shape[1:], spacing)
+        else:
+            g = _grid(shape, spacing)
+        st = gd_stats()
+        _check(lib().gd_generalized_geodesic_batched(
+            C.byref(g), int(batch or 1), C.c_void_p(image.data_ptr()),
+            C.c_void_p(soft_mask.data_ptr()), lam, nu, iterations, C.c_void_p(out.data_ptr()),
+            GD_MEM_DEVICE, device._stream(stream), C.byref(st)))
+        return st
+
+    @staticmethod
+    def gsf(image, soft_mask, out, spacing=None, lam=1.0, nu=1e10, iterations=2, theta=0.0,
+            stream=None):
+        g = _grid(tuple(image.shape), spacing)
+        st = gd_stats()
+        _check(lib().gd_gsf(C.byref(g), C.c_void_p(image.data_ptr()),
+                            C.c_void_p(soft_mask.data_ptr()), lam, nu, iterations, theta,
+                            C.c_void_p(out.data_ptr()), GD_MEM_DEVICE, device._stream(stream),
+                            C.byref(st)))
+        return st
+
+    @staticmethod
+    def parallel_scan(image, dist, spacing=None, lam=1.0, iterations=2, stream=None):
+        g = _grid(tuple(image.shape), spacing)
+        _check(lib().gd_parallel_scan(C.byref(g), C.c_void_p(image.data_ptr()),
+                                      C.c_void_p(dist.data_ptr()), lam, iterations,
+                                      GD_MEM_DEVICE, device._stream(stream)))
+
+    @staticmethod
+    def fill_splitmix(out, seed: int, stream=None):
+        _check(lib().gd_fill_splitmix(C.c_void_p(out.data_ptr()), out.numel(),
+                                      C.c_ulonglong(seed), device._stream(stream)))

@@ -1,0 +1,39 @@
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace gdb {
+
+// A batch of B volumes of logical extent (D, H, W) in a pitched layout:
+// element (b, a0, a1, a2) lives at b*vol + a0*zs + a1*ys + a2, where
+// (a0, a1, a2) = (z, y, x) for the canonical layout and (x, z, y) for the
+// x-sweep layout.  Element kernels always enumerate canonical (z, y, x).
+struct VolView {
+    int B = 1, D = 1, H = 1, W = 1;
+    long long vol = 0, zs = 0, ys = 0;
+    __host__ __device__ long long count() const {
+        return static_cast<long long>(B) * D * H * W;
+    }
+};
+
+struct ImageCheck {
+    int emax, tmin, pos, neg, bad_mask, nonfinite;
+};
+
+cudaError_t launch_init_generalized(const VolView& m, const VolView& d, const float* mask,
+                                    float* dist, double nu, cudaStream_t s);
+cudaError_t launch_transpose(const VolView& src_v, const VolView& dst_v, const float* src,
+                             float* dst, bool forward, cudaStream_t s);
+cudaError_t launch_image_check(const VolView& v, const float* img, const float* mask,
+                               ImageCheck* out, cudaStream_t s);
+cudaError_t launch_gsf_sources(const VolView& v, const float* mask, const VolView& o, float* out,
+                               cudaStream_t s);
+cudaError_t launch_gsf_dilate(const VolView& v, const float* dist, float* out, double theta,
+                              unsigned long long* n_complement, cudaStream_t s);
+cudaError_t launch_gsf_erode(const VolView& v, const float* dist, const VolView& o, float* out,
+                             double theta, cudaStream_t s);
+cudaError_t launch_max_change(const VolView& v, const float* before, const float* after,
+                              unsigned long long* out, cudaStream_t s);
+cudaError_t launch_splitmix(float* out, long long n, unsigned long long seed, cudaStream_t s);
+
+}  // namespace gdb

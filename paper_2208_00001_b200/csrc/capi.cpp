@@ -1,0 +1,211 @@
+// extern "C" boundary (include/geodist_b200.h) over the device engine.
+// Host-memory calls stage through cached device buffers and synchronise, the
+// way the reference's calls block; device-memory calls enqueue on the caller's
+// stream.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/geodist_b200.h"
+#include "engine.cuh"
+
+namespace {
+
+thread_local std::string t_err;
+
+int fail(const gdb::Status& s) {
+    t_err = s.msg;
+    return s.code;
+}
+
+int fail(int code, const std::string& m) {
+    t_err = m;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    t_err = std::string(what) + ": " + cudaGetErrorString(e);
+    return GD_CUDA_ERROR;
+}
+
+struct HostStage {
+    std::mutex mu;
+    void* p[3] = {nullptr, nullptr, nullptr};
+    size_t n[3] = {0, 0, 0};
+    bool ensure(int i, size_t bytes) {
+        if (bytes <= n[i]) return true;
+        if (p[i]) cudaFree(p[i]);
+        p[i] = nullptr;
+        n[i] = 0;
+        if (cudaMalloc(&p[i], bytes) != cudaSuccess) return false;
+        n[i] = bytes;
+        return true;
+    }
+};
+
+HostStage& stage() {
+    static HostStage st[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return st[dev & 63];
+}
+
+int check_device() {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        return fail(GD_CUDA_ERROR, "no CUDA device available (geodist_b200 has no CPU fallback)");
+    return GD_OK;
+}
+
+void fill_stats(gd_stats* out, const gdb::ScanStats& st) {
+    if (!out) return;
+    out->rounds = st.rounds;
+    out->converged = st.converged ? 1 : 0;
+    out->complement_empty = st.complement_empty ? 1 : 0;
+    out->last_change = st.last_change;
+    out->kernel_launches = st.kernel_launches;
+}
+
+int grid_of(const gd_grid* g, gdb::GridDesc* d) {
+    if (!g) return fail(GD_INVALID_ARGUMENT, "null grid");
+    gdb::Status s = gdb::make_grid_desc(g->ndim, g->dims, g->spacing, d);
+    return s.ok() ? GD_OK : fail(s);
+}
+
+// Runs `fn(img, aux, io, stream)` on device pointers, staging host buffers.
+// n_in_img/n_in_aux/n_io are element counts; io_in: copy io in before the call.
+template <class F>
+int run(int mem, void* stream, long long n, const float* img, const float* aux, float* io,
+        bool io_in, F&& fn) {
+    if (int rc = check_device()) return rc;
+    if (mem == GD_MEM_DEVICE) {
+        gdb::Status s = fn(img, aux, io, static_cast<cudaStream_t>(stream));
+        return s.ok() ? GD_OK : fail(s);
+    }
+    if (mem != GD_MEM_HOST) return fail(GD_INVALID_ARGUMENT, "mem must be GD_MEM_HOST or GD_MEM_DEVICE");
+    HostStage& hs = stage();
+    std::lock_guard<std::mutex> lk(hs.mu);
+    const size_t bytes = static_cast<size_t>(n) * sizeof(float);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!hs.ensure(0, bytes) || !hs.ensure(1, bytes) || !hs.ensure(2, bytes))
+        return fail(GD_CUDA_ERROR, "device allocation failed");
+    float* d_img = static_cast<float*>(hs.p[0]);
+    float* d_aux = static_cast<float*>(hs.p[1]);
+    float* d_io = static_cast<float*>(hs.p[2]);
+    cudaError_t e;
+    if (img && (e = cudaMemcpyAsync(d_img, img, bytes, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+        return cuda_fail(e, "H2D image");
+    if (aux && (e = cudaMemcpyAsync(d_aux, aux, bytes, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+        return cuda_fail(e, "H2D mask");
+    if (io_in && (e = cudaMemcpyAsync(d_io, io, bytes, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+        return cuda_fail(e, "H2D dist");
+    gdb::Status st = fn(img ? d_img : nullptr, aux ? d_aux : nullptr, d_io, s);
+    if (!st.ok()) {
+        cudaStreamSynchronize(s);
+        return fail(st);
+    }
+    if ((e = cudaMemcpyAsync(io, d_io, bytes, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+        return cuda_fail(e, "D2H result");
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "stream sync");
+    return GD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gd_last_error(void) { return t_err.c_str(); }
+int gd_version(void) { return GD_VERSION; }
+long long gd_kernel_launches(void) { return gdb::kernel_launch_count(); }
+
+int gd_set_exact_blend(int on) {
+    gdb::set_exact_blend(on != 0);
+    return GD_OK;
+}
+
+int gd_generalized_geodesic_batched(const gd_grid* grid, int batch, const float* images,
+                                    const float* soft_masks, double lambda, double nu,
+                                    int iterations, float* out, int mem, void* stream,
+                                    gd_stats* stats) {
+    gdb::GridDesc g;
+    if (int rc = grid_of(grid, &g)) return rc;
+    if (batch < 1) return fail(GD_INVALID_ARGUMENT, "batch must be >= 1");
+    if (!images || !soft_masks || !out) return fail(GD_INVALID_ARGUMENT, "null buffer");
+    gdb::ScanStats st;
+    int rc = run(mem, stream, g.voxels() * batch, images, soft_masks, out, false,
+                 [&](const float* i, const float* m, float* o, cudaStream_t s) {
+                     return gdb::generalized_geodesic(g, batch, i, m, o, lambda, nu, iterations,
+                                                      s, &st);
+                 });
+    fill_stats(stats, st);
+    return rc;
+}
+
+int gd_generalized_geodesic(const gd_grid* grid, const float* image, const float* soft_mask,
+                            double lambda, double nu, int iterations, float* out, int mem,
+                            void* stream, gd_stats* stats) {
+    return gd_generalized_geodesic_batched(grid, 1, image, soft_mask, lambda, nu, iterations, out,
+                                           mem, stream, stats);
+}
+
+int gd_gsf(const gd_grid* grid, const float* image, const float* soft_mask, double lambda,
+           double nu, int iterations, double theta, float* out, int mem, void* stream,
+           gd_stats* stats) {
+    gdb::GridDesc g;
+    if (int rc = grid_of(grid, &g)) return rc;
+    if (!image || !soft_mask || !out) return fail(GD_INVALID_ARGUMENT, "null buffer");
+    gdb::ScanStats st;
+    int rc = run(mem, stream, g.voxels(), image, soft_mask, out, false,
+                 [&](const float* i, const float* m, float* o, cudaStream_t s) {
+                     return gdb::gsf(g, i, m, o, lambda, nu, iterations, theta, s, &st);
+                 });
+    fill_stats(stats, st);
+    return rc;
+}
+
+int gd_directional_pass(const gd_grid* grid, const float* image, float* dist, int axis,
+                        int orientation, double lambda, int mem, void* stream) {
+    gdb::GridDesc g;
+    if (int rc = grid_of(grid, &g)) return rc;
+    if (!image || !dist) return fail(GD_INVALID_ARGUMENT, "null buffer");
+    return run(mem, stream, g.voxels(), image, nullptr, dist, true,
+               [&](const float* i, const float*, float* d, cudaStream_t s) {
+                   return gdb::directional_pass(g, 1, i, d, axis, orientation, lambda, s, nullptr);
+               });
+}
+
+int gd_parallel_scan(const gd_grid* grid, const float* image, float* dist, double lambda,
+                     int iterations, int mem, void* stream) {
+    gdb::GridDesc g;
+    if (int rc = grid_of(grid, &g)) return rc;
+    if (!image || !dist) return fail(GD_INVALID_ARGUMENT, "null buffer");
+    return run(mem, stream, g.voxels(), image, nullptr, dist, true,
+               [&](const float* i, const float*, float* d, cudaStream_t s) {
+                   return gdb::parallel_scan(g, 1, i, d, lambda, iterations, s, nullptr);
+               });
+}
+
+int gd_scan_to_fixpoint(const gd_grid* grid, const float* image, float* dist, double lambda,
+                        int max_rounds, double tol, int mem, void* stream, gd_stats* stats) {
+    gdb::GridDesc g;
+    if (int rc = grid_of(grid, &g)) return rc;
+    if (!image || !dist) return fail(GD_INVALID_ARGUMENT, "null buffer");
+    gdb::ScanStats st;
+    int rc = run(mem, stream, g.voxels(), image, nullptr, dist, true,
+                 [&](const float* i, const float*, float* d, cudaStream_t s) {
+                     return gdb::scan_to_fixpoint(g, i, d, lambda, max_rounds, tol, s, &st);
+                 });
+    fill_stats(stats, st);
+    return rc;
+}
+
+int gd_fill_splitmix(float* device_out, long long n, unsigned long long seed, void* stream) {
+    if (int rc = check_device()) return rc;
+    gdb::Status s = gdb::fill_splitmix(device_out, n, seed, static_cast<cudaStream_t>(stream));
+    return s.ok() ? GD_OK : fail(s);
+}
+
+}  // extern "C"

@@ -1,0 +1,573 @@
+// Host engine: per-(device, stream) scratch, TMA descriptors, the pass
+// scheduler and the transforms.  See engine.cuh.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+
+#include "aux_kernels.cuh"
+#include "engine.cuh"
+#include "metric_host.hpp"
+#include "sweep.cuh"
+
+namespace gdb {
+
+namespace {
+
+std::atomic<long long> g_launches{0};
+std::atomic<bool> g_exact_blend{false};
+
+Status cuda_status(cudaError_t e, const char* what) {
+    return {kCudaError, std::string(what) + ": " + cudaGetErrorString(e)};
+}
+
+#define GD_CK(x)                                              \
+    do {                                                      \
+        cudaError_t e_ = (x);                                 \
+        if (e_ != cudaSuccess) return cuda_status(e_, #x);    \
+    } while (0)
+#define GD_ST(x)                     \
+    do {                             \
+        Status s_ = (x);             \
+        if (!s_.ok()) return s_;     \
+    } while (0)
+
+struct Buf {
+    void* p = nullptr;
+    size_t n = 0;
+    Status ensure(size_t bytes) {
+        if (bytes <= n) return Status::Ok();
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+        GD_CK(cudaMalloc(&p, bytes));
+        n = bytes;
+        return Status::Ok();
+    }
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+struct StreamCtx {
+    Buf halo;
+    size_t halo_bytes_zeroed = 0;
+    uint32_t tag = 1;  // 0 never matches: freshly zeroed halo words are stale
+    Buf dT, iT, padI, padD, tmp, small;
+};
+
+struct DeviceCtx {
+    std::mutex mu;
+    std::map<cudaStream_t, StreamCtx> streams;
+};
+
+DeviceCtx& device_ctx() {
+    static DeviceCtx ctx[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return ctx[dev & 63];
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+Status make_map(CUtensorMap* m, const float* base, const uint64_t dims[4],
+                const uint64_t strides_bytes[3], const uint32_t box[4]) {
+    auto fn = encode_fn();
+    if (!fn) return {kCudaError, "cuTensorMapEncodeTiled unavailable"};
+    const cuuint32_t es[4] = {1, 1, 1, 1};
+    cuuint64_t gd[4] = {dims[0], dims[1], dims[2], dims[3]};
+    cuuint64_t gs[3] = {strides_bytes[0], strides_bytes[1], strides_bytes[2]};
+    cuuint32_t bx[4] = {box[0], box[1], box[2], box[3]};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), gd, gs, bx,
+                    es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return {kCudaError, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")"};
+    return Status::Ok();
+}
+
+int round4(int x) { return (x + 3) & ~3; }
+
+// The volumes a scan works on: canonical pitched layout (row pitch Wp) plus
+// the x-sweep layout [b][x][z][y] (row pitch Hp).
+struct Work {
+    GridDesc g;
+    int B = 1;
+    const float* img = nullptr;
+    float* dist = nullptr;
+    int Wp = 0;
+    long long zs = 0, vol = 0;
+    float* dT = nullptr;
+    float* iT = nullptr;
+    int Hp = 0;
+    long long volT = 0;
+    bool iT_ready = false;
+
+    VolView canon() const {
+        VolView v;
+        v.B = B; v.D = g.D; v.H = g.H; v.W = g.W;
+        v.vol = vol; v.zs = zs; v.ys = Wp;
+        return v;
+    }
+    VolView trans() const {
+        VolView v;
+        v.B = B; v.D = g.D; v.H = g.H; v.W = g.W;
+        v.vol = volT; v.zs = static_cast<long long>(g.D) * Hp; v.ys = Hp;
+        return v;
+    }
+};
+
+int cost_kind(double lambda) {
+    // scan_common.hpp:17-21: exact compare
+    if (lambda == 0.0) return kSpatial;
+    if (lambda == 1.0) return kIntensity;
+    return kBlend;
+}
+
+struct Prepared {
+    bool exact_diff = true;  // every |I_p - I_q| exact in f32
+    bool mask_ok = true;
+};
+
+Status check_inputs(StreamCtx& sc, const Work& w, const float* mask, bool want_img,
+                    cudaStream_t s, Prepared* out) {
+    GD_ST(sc.small.ensure(256));
+    ImageCheck* dev = sc.small.as<ImageCheck>();
+    VolView v = w.canon();
+    GD_CK(launch_image_check(v, want_img ? w.img : nullptr, mask, dev, s));
+    ++g_launches;
+    ImageCheck h;
+    GD_CK(cudaMemcpyAsync(&h, dev, sizeof(h), cudaMemcpyDeviceToHost, s));
+    GD_CK(cudaStreamSynchronize(s));
+    out->mask_ok = h.bad_mask == 0;
+    if (h.nonfinite) {
+        out->exact_diff = false;
+    } else if (h.emax < -999) {
+        out->exact_diff = true;  // all zeros
+    } else {
+        const int limit = (h.pos && h.neg) ? 22 : 23;
+        out->exact_diff = (h.emax - h.tmin) <= limit;
+    }
+    return Status::Ok();
+}
+
+Status ensure_x_layout(StreamCtx& sc, Work& w, bool need_img, cudaStream_t s) {
+    w.Hp = round4(w.g.H);
+    w.volT = static_cast<long long>(w.g.W) * w.g.D * w.Hp;
+    const size_t bytes = static_cast<size_t>(w.B) * w.volT * sizeof(float);
+    GD_ST(sc.dT.ensure(bytes));
+    w.dT = sc.dT.as<float>();
+    if (need_img && !w.iT_ready) {
+        GD_ST(sc.iT.ensure(bytes));
+        w.iT = sc.iT.as<float>();
+        GD_CK(launch_transpose(w.canon(), w.trans(), w.img, w.iT, true, s));
+        ++g_launches;
+        w.iT_ready = true;
+    }
+    return Status::Ok();
+}
+
+// One launch group of the persistent sweep kernel: `npass` passes along
+// `axis` (canonical 0/1; 2 = the x axis in the [b][x][z][y] layout).
+Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int npass,
+                 double lambda, bool f64, cudaStream_t s, ScanStats* st) {
+    const GridDesc& g = w.g;
+    int ns, nu, nv, sweep_dim;
+    long long ss, su, vol;
+    const float* ibase;
+    float* dbase;
+    uint64_t dims[4], strides[3];
+    if (axis == 0) {
+        ns = g.D; nu = g.H; nv = g.W; ss = w.zs; su = w.Wp; vol = w.vol;
+        ibase = w.img; dbase = w.dist; sweep_dim = 2;
+        dims[0] = g.W; dims[1] = g.H; dims[2] = g.D;
+        strides[0] = w.Wp * 4ull; strides[1] = w.zs * 4ull; strides[2] = w.vol * 4ull;
+    } else if (axis == 1) {
+        ns = g.H; nu = g.D; nv = g.W; ss = w.Wp; su = w.zs; vol = w.vol;
+        ibase = w.img; dbase = w.dist; sweep_dim = 1;
+        dims[0] = g.W; dims[1] = g.H; dims[2] = g.D;
+        strides[0] = w.Wp * 4ull; strides[1] = w.zs * 4ull; strides[2] = w.vol * 4ull;
+    } else {
+        ns = g.W; nu = g.D; nv = g.H; ss = static_cast<long long>(g.D) * w.Hp; su = w.Hp;
+        vol = w.volT; ibase = w.iT; dbase = w.dT; sweep_dim = 2;
+        dims[0] = g.H; dims[1] = g.D; dims[2] = g.W;
+        strides[0] = w.Hp * 4ull; strides[1] = static_cast<uint64_t>(g.D) * w.Hp * 4ull;
+        strides[2] = w.volT * 4ull;
+    }
+    if (ns < 2) return Status::Ok();  // scan_parallel.cpp:308-310
+    const int kind = cost_kind(lambda);
+    if (kind == kSpatial) ibase = dbase;  // intensities never read; any valid map will do
+    const int R = nu == 1 ? 1 : 4;
+    const int NWU = nu == 1 ? 1 : 8;
+    const int TU = R * NWU;
+    const int ntu = (nu + TU - 1) / TU;
+    const int ntv = (nv + kTV - 1) / kTV;
+    const long long per_vol = static_cast<long long>(ntu) * ntv;
+    const int maxc = sweep_max_coresident(R, NWU, kind, f64);
+    if (maxc <= 0) return {kCudaError, "sweep kernel cannot be resident on this device"};
+    if (per_vol > maxc)
+        return {kUnsupported, "plane of " + std::to_string(nu) + "x" + std::to_string(nv) +
+                                  " needs " + std::to_string(per_vol) + " co-resident tiles (max " +
+                                  std::to_string(maxc) + ")"};
+    const int group = static_cast<int>(std::min<long long>(w.B, maxc / per_vol));
+    const int HALO_N = 2 * kTV + 2 * TU;
+    const int J = npass * (ns - 1);
+
+    SweepParams p{};
+    p.ss = ss; p.su = su; p.vol_stride = vol;
+    p.ns = ns; p.nu = nu; p.nv = nv; p.ntu = ntu; p.ntv = ntv;
+    p.tma_sweep_dim = sweep_dim;
+    p.first_orient = first_orient;
+    p.npass = npass;
+    p.fence_turn = npass == 2 ? 1 : 0;
+    p.lambda = lambda;
+    p.lambda_f = static_cast<float>(lambda);
+    for (int du = -1; du <= 1; ++du)
+        for (int dv = -1; dv <= 1; ++dv) {
+            int dz, dy, dx;
+            if (axis == 0) { dz = -first_orient; dy = du; dx = dv; }
+            else if (axis == 1) { dz = du; dy = -first_orient; dx = dv; }
+            else { dz = du; dy = dv; dx = -first_orient; }
+            const double rho = offset_rho(dz, dy, dx, g.sz, g.sy, g.sx);
+            const int k = (du + 1) * 3 + (dv + 1);
+            p.rho[k] = rho;
+            p.c0[k] = blend_c0(lambda, rho);
+            p.c0_f[k] = static_cast<float>(p.c0[k]);
+        }
+
+    uint32_t box_d[4], box_i[4];
+    if (sweep_dim == 2) {
+        box_d[0] = kTV; box_d[1] = TU; box_d[2] = 1; box_d[3] = 1;
+        box_i[0] = kIW; box_i[1] = TU + 2; box_i[2] = 1; box_i[3] = 1;
+    } else {
+        box_d[0] = kTV; box_d[1] = 1; box_d[2] = TU; box_d[3] = 1;
+        box_i[0] = kIW; box_i[1] = 1; box_i[2] = TU + 2; box_i[3] = 1;
+    }
+
+    for (int b0 = 0; b0 < w.B; b0 += group) {
+        const int nvol = std::min(group, w.B - b0);
+        dims[3] = static_cast<uint64_t>(nvol);
+        CUtensorMap tm_d, tm_i;
+        GD_ST(make_map(&tm_d, dbase + b0 * vol, dims, strides, box_d));
+        GD_ST(make_map(&tm_i, ibase + b0 * vol, dims, strides, box_i));
+        const size_t words = static_cast<size_t>(nvol) * per_vol * 2 * HALO_N;
+        GD_ST(sc.halo.ensure(words * 8));
+        if (sc.halo_bytes_zeroed < sc.halo.n) {
+            GD_CK(cudaMemsetAsync(sc.halo.p, 0, sc.halo.n, s));
+            sc.halo_bytes_zeroed = sc.halo.n;
+            sc.tag = 1;
+        }
+        if (static_cast<uint64_t>(sc.tag) + J + 2 >= 0xffffffffull) {
+            GD_CK(cudaMemsetAsync(sc.halo.p, 0, sc.halo.n, s));
+            sc.tag = 1;
+        }
+        p.dist = dbase + b0 * vol;
+        p.nvol = nvol;
+        p.halo = sc.halo.as<unsigned long long>();
+        p.tag_base = sc.tag;
+        sc.tag += static_cast<uint32_t>(J + 1);
+        GD_CK(launch_sweep(kind, f64, R, NWU, tm_d, tm_i, p, s));
+        ++g_launches;
+        if (st) ++st->kernel_launches;
+    }
+    return Status::Ok();
+}
+
+Status x_pair(StreamCtx& sc, Work& w, int first_orient, int npass, double lambda, bool f64,
+              cudaStream_t s, ScanStats* st) {
+    GD_ST(ensure_x_layout(sc, w, lambda != 0.0, s));
+    GD_CK(launch_transpose(w.canon(), w.trans(), w.dist, w.dT, true, s));
+    ++g_launches;
+    GD_ST(run_sweep(sc, w, 2, first_orient, npass, lambda, f64, s, st));
+    GD_CK(launch_transpose(w.trans(), w.canon(), w.dT, w.dist, false, s));
+    ++g_launches;
+    return Status::Ok();
+}
+
+bool pick_f64(int kind, const Prepared& prep) {
+    if (kind == kIntensity) return !prep.exact_diff;
+    if (kind == kBlend) return g_exact_blend.load();
+    return false;
+}
+
+// parallel_scan_inplace: for it: FB BF (3D) TB BT LR RL  (metric.cpp:35-44)
+Status scan_work(StreamCtx& sc, Work& w, double lambda, int iterations, bool f64,
+                 cudaStream_t s, ScanStats* st) {
+    for (int it = 0; it < iterations; ++it) {
+        if (w.g.ndim == 3) GD_ST(run_sweep(sc, w, 0, +1, 2, lambda, f64, s, st));
+        GD_ST(run_sweep(sc, w, 1, +1, 2, lambda, f64, s, st));
+        if (w.g.W >= 2) GD_ST(x_pair(sc, w, +1, 2, lambda, f64, s, st));
+    }
+    if (st) st->rounds += iterations;
+    return Status::Ok();
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// Sets up w.img / w.dist: the caller's buffers when the layout is TMA-legal
+// (W % 4 == 0, 16-byte aligned), else padded copies (copy_in: dist content).
+Status bind(StreamCtx& sc, Work& w, const GridDesc& g, int B, const float* img, float* dist,
+            bool copy_dist_in, cudaStream_t s, bool* padded) {
+    w.g = g;
+    w.B = B;
+    const bool direct = (g.W % 4 == 0) && aligned16(img) && aligned16(dist);
+    w.Wp = direct ? g.W : round4(g.W);
+    w.zs = static_cast<long long>(g.H) * w.Wp;
+    w.vol = static_cast<long long>(g.D) * w.zs;
+    *padded = !direct;
+    if (direct) {
+        w.img = img;
+        w.dist = dist;
+        return Status::Ok();
+    }
+    const size_t bytes = static_cast<size_t>(B) * w.vol * sizeof(float);
+    GD_ST(sc.padI.ensure(bytes));
+    GD_ST(sc.padD.ensure(bytes));
+    const size_t rows = static_cast<size_t>(B) * g.D * g.H;
+    if (img) {
+        GD_CK(cudaMemcpy2DAsync(sc.padI.p, w.Wp * 4, img, g.W * 4, g.W * 4, rows,
+                                cudaMemcpyDeviceToDevice, s));
+    }
+    if (copy_dist_in) {
+        GD_CK(cudaMemcpy2DAsync(sc.padD.p, w.Wp * 4, dist, g.W * 4, g.W * 4, rows,
+                                cudaMemcpyDeviceToDevice, s));
+    }
+    w.img = img ? sc.padI.as<float>() : nullptr;
+    w.dist = sc.padD.as<float>();
+    return Status::Ok();
+}
+
+Status unbind(const Work& w, float* dist, cudaStream_t s) {
+    const size_t rows = static_cast<size_t>(w.B) * w.g.D * w.g.H;
+    GD_CK(cudaMemcpy2DAsync(dist, w.g.W * 4, w.dist, w.Wp * 4, w.g.W * 4, rows,
+                            cudaMemcpyDeviceToDevice, s));
+    return Status::Ok();
+}
+
+Status validate_params(double lambda, double nu, int iterations) {
+    // TransformParams::validate (grid.cpp:67-78)
+    if (!(lambda >= 0.0 && lambda <= 1.0))
+        return Status::Invalid("lambda must lie in [0, 1], got " + std::to_string(lambda));
+    if (!(nu >= 0.0)) return Status::Invalid("nu must be >= 0, got " + std::to_string(nu));
+    if (iterations < 1)
+        return Status::Invalid("iterations must be >= 1, got " + std::to_string(iterations));
+    return Status::Ok();
+}
+
+Status generalized_locked(StreamCtx& sc, const GridDesc& g, int B, const float* img,
+                          const float* mask, float* out, double lambda, double nu, int iterations,
+                          cudaStream_t s, ScanStats* st) {
+    GD_ST(validate_params(lambda, nu, iterations));
+    Work w;
+    bool padded = false;
+    GD_ST(bind(sc, w, g, B, img, out, false, s, &padded));
+    const int kind = cost_kind(lambda);
+    Prepared prep;
+    // mask range is checked on the caller's (dense) mask; image on the working copy.
+    {
+        Work wm = w;
+        wm.Wp = g.W;
+        wm.zs = static_cast<long long>(g.H) * g.W;
+        wm.vol = static_cast<long long>(g.D) * wm.zs;
+        wm.img = img;
+        GD_ST(check_inputs(sc, wm, mask, kind == kIntensity, s, &prep));
+    }
+    if (!prep.mask_ok)
+        return Status::Invalid("generalized_geodesic: mask values must lie in [0, 1]");
+    VolView mv;
+    mv.B = B; mv.D = g.D; mv.H = g.H; mv.W = g.W;
+    mv.zs = static_cast<long long>(g.H) * g.W; mv.ys = g.W; mv.vol = g.D * mv.zs;
+    GD_CK(launch_init_generalized(mv, w.canon(), mask, w.dist, nu, s));
+    ++g_launches;
+    GD_ST(scan_work(sc, w, lambda, iterations, pick_f64(kind, prep), s, st));
+    if (padded) GD_ST(unbind(w, out, s));
+    return Status::Ok();
+}
+
+}  // namespace
+
+Status make_grid_desc(int ndim, const int* dims, const double* spacing, GridDesc* out) {
+    if (ndim != 2 && ndim != 3)
+        return Status::Invalid("grid rank must be 2 or 3, got " + std::to_string(ndim));
+    GridDesc g;
+    g.ndim = ndim;
+    int cd[3] = {1, 1, 1};
+    double cs[3] = {1.0, 1.0, 1.0};
+    for (int a = 0; a < ndim; ++a) {
+        if (dims[a] < 1)
+            return Status::Invalid("grid extent must be >= 1, got " + std::to_string(dims[a]));
+        if (!(spacing[a] > 0.0) || !std::isfinite(spacing[a]))
+            return Status::Invalid("grid spacing must be finite and > 0, got " +
+                                   std::to_string(spacing[a]));
+        cd[a + 3 - ndim] = dims[a];
+        cs[a + 3 - ndim] = spacing[a];
+    }
+    g.D = cd[0]; g.H = cd[1]; g.W = cd[2];
+    g.sz = cs[0]; g.sy = cs[1]; g.sx = cs[2];
+    *out = g;
+    return Status::Ok();
+}
+
+void set_exact_blend(bool on) { g_exact_blend.store(on); }
+bool exact_blend() { return g_exact_blend.load(); }
+long long kernel_launch_count() { return g_launches.load(); }
+
+Status directional_pass(const GridDesc& g, int B, const float* img, float* dist, int axis,
+                        int orientation, double lambda, cudaStream_t s, ScanStats* st) {
+    GD_ST(validate_params(lambda, 0.0, 1));
+    const bool dir_ok = (orientation == 1 || orientation == -1) &&
+                        (g.ndim == 2 ? (axis == 1 || axis == 2) : (axis >= 0 && axis <= 2));
+    if (!dir_ok) return Status::Invalid("invalid pass direction for rank " + std::to_string(g.ndim));
+    DeviceCtx& dc = device_ctx();
+    std::lock_guard<std::mutex> lk(dc.mu);
+    StreamCtx& sc = dc.streams[s];
+    Work w;
+    bool padded = false;
+    GD_ST(bind(sc, w, g, B, img, dist, true, s, &padded));
+    const int kind = cost_kind(lambda);
+    Prepared prep;
+    if (kind == kIntensity) GD_ST(check_inputs(sc, w, nullptr, true, s, &prep));
+    const bool f64 = pick_f64(kind, prep);
+    if (axis == 2) {
+        if (g.W >= 2) GD_ST(x_pair(sc, w, orientation, 1, lambda, f64, s, st));
+    } else {
+        GD_ST(run_sweep(sc, w, axis, orientation, 1, lambda, f64, s, st));
+    }
+    if (padded) GD_ST(unbind(w, dist, s));
+    return Status::Ok();
+}
+
+Status parallel_scan(const GridDesc& g, int B, const float* img, float* dist, double lambda,
+                     int iterations, cudaStream_t s, ScanStats* st) {
+    GD_ST(validate_params(lambda, 0.0, iterations));
+    DeviceCtx& dc = device_ctx();
+    std::lock_guard<std::mutex> lk(dc.mu);
+    StreamCtx& sc = dc.streams[s];
+    Work w;
+    bool padded = false;
+    GD_ST(bind(sc, w, g, B, img, dist, true, s, &padded));
+    const int kind = cost_kind(lambda);
+    Prepared prep;
+    if (kind == kIntensity) GD_ST(check_inputs(sc, w, nullptr, true, s, &prep));
+    GD_ST(scan_work(sc, w, lambda, iterations, pick_f64(kind, prep), s, st));
+    if (padded) GD_ST(unbind(w, dist, s));
+    return Status::Ok();
+}
+
+Status generalized_geodesic(const GridDesc& g, int B, const float* img, const float* mask,
+                            float* out, double lambda, double nu, int iterations, cudaStream_t s,
+                            ScanStats* st) {
+    DeviceCtx& dc = device_ctx();
+    std::lock_guard<std::mutex> lk(dc.mu);
+    StreamCtx& sc = dc.streams[s];
+    return generalized_locked(sc, g, B, img, mask, out, lambda, nu, iterations, s, st);
+}
+
+Status gsf(const GridDesc& g, const float* img, const float* mask, float* out, double lambda,
+           double nu, int iterations, double theta, cudaStream_t s, ScanStats* st) {
+    GD_ST(validate_params(lambda, nu, iterations));
+    if (!(theta >= 0.0)) return Status::Invalid("theta must be >= 0, got " + std::to_string(theta));
+    DeviceCtx& dc = device_ctx();
+    std::lock_guard<std::mutex> lk(dc.mu);
+    StreamCtx& sc = dc.streams[s];
+    const long long n = g.voxels();
+    const size_t bytes = static_cast<size_t>(n) * sizeof(float);
+    GD_ST(sc.tmp.ensure(bytes));
+    GD_ST(sc.small.ensure(256));
+    float* tmp = sc.tmp.as<float>();
+    VolView v;
+    v.D = g.D; v.H = g.H; v.W = g.W; v.ys = g.W; v.zs = static_cast<long long>(g.H) * g.W;
+    v.vol = g.D * v.zs;
+    // geodesic_dilate (transforms.cpp:185-202)
+    GD_CK(launch_gsf_sources(v, mask, v, tmp, s));
+    ++g_launches;
+    GD_ST(generalized_locked(sc, g, 1, img, tmp, out, lambda, nu, iterations, s, st));
+    unsigned long long* cnt = reinterpret_cast<unsigned long long*>(sc.small.as<char>() + 128);
+    GD_CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), s));
+    GD_CK(launch_gsf_dilate(v, out, out, theta, cnt, s));
+    ++g_launches;
+    unsigned long long n_src = 0;
+    GD_CK(cudaMemcpyAsync(&n_src, cnt, sizeof(n_src), cudaMemcpyDeviceToHost, s));
+    GD_CK(cudaStreamSynchronize(s));
+    // geodesic_erode (transforms.cpp:204-229)
+    if (n_src == 0) {
+        if (st) st->complement_empty = true;
+        return Status::Ok();  // out already holds K = threshold(dilated)
+    }
+    GD_ST(generalized_locked(sc, g, 1, img, out, tmp, lambda, nu, iterations, s, st));
+    GD_CK(launch_gsf_erode(v, tmp, v, out, theta, s));
+    ++g_launches;
+    return Status::Ok();
+}
+
+Status scan_to_fixpoint(const GridDesc& g, const float* img, float* dist, double lambda,
+                        int max_rounds, double tol, cudaStream_t s, ScanStats* st) {
+    GD_ST(validate_params(lambda, 0.0, 1));
+    if (max_rounds < 1)
+        return Status::Invalid("max_rounds must be >= 1, got " + std::to_string(max_rounds));
+    if (!(tol >= 0.0)) return Status::Invalid("tol must be >= 0");
+    DeviceCtx& dc = device_ctx();
+    std::lock_guard<std::mutex> lk(dc.mu);
+    StreamCtx& sc = dc.streams[s];
+    Work w;
+    bool padded = false;
+    GD_ST(bind(sc, w, g, 1, img, dist, true, s, &padded));
+    const int kind = cost_kind(lambda);
+    Prepared prep;
+    if (kind == kIntensity) GD_ST(check_inputs(sc, w, nullptr, true, s, &prep));
+    const bool f64 = pick_f64(kind, prep);
+    const size_t bytes = static_cast<size_t>(w.vol) * sizeof(float);
+    GD_ST(sc.tmp.ensure(bytes));
+    GD_ST(sc.small.ensure(256));
+    unsigned long long* chg = reinterpret_cast<unsigned long long*>(sc.small.as<char>() + 192);
+    ScanStats local;
+    ScanStats* stp = st ? st : &local;
+    stp->converged = false;
+    int rounds = 0;
+    double last = 0.0;
+    while (rounds < max_rounds) {
+        GD_CK(cudaMemcpyAsync(sc.tmp.p, w.dist, bytes, cudaMemcpyDeviceToDevice, s));
+        GD_ST(scan_work(sc, w, lambda, 1, f64, s, nullptr));
+        ++rounds;
+        GD_CK(cudaMemsetAsync(chg, 0, sizeof(unsigned long long), s));
+        GD_CK(launch_max_change(w.canon(), sc.tmp.as<float>(), w.dist, chg, s));
+        ++g_launches;
+        unsigned long long bits = 0;
+        GD_CK(cudaMemcpyAsync(&bits, chg, sizeof(bits), cudaMemcpyDeviceToHost, s));
+        GD_CK(cudaStreamSynchronize(s));
+        std::memcpy(&last, &bits, sizeof(last));
+        if (last <= tol) {
+            stp->converged = true;
+            break;
+        }
+    }
+    stp->rounds += rounds;
+    stp->last_change = last;
+    if (padded) GD_ST(unbind(w, dist, s));
+    return Status::Ok();
+}
+
+Status fill_splitmix(float* out, long long n, unsigned long long seed, cudaStream_t s) {
+    GD_CK(launch_splitmix(out, n, seed, s));
+    ++g_launches;
+    return Status::Ok();
+}
+
+}  // namespace gdb

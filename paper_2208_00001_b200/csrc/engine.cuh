@@ -1,0 +1,80 @@
+// Host-side engine: per-device context, pass scheduler, transforms.
+// All entry points take DEVICE pointers to B dense canonical volumes
+// ([b][z][y][x], x fastest) and enqueue on `stream`; the C-ABI (capi.cpp)
+// adds host-memory staging and the C++ drop-in (geodist_api.cpp) sits on top.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+
+namespace gdb {
+
+enum StatusCode : int {
+    kOk = 0,
+    kInvalidArgument = 1,  // std::invalid_argument in the reference
+    kEmptySeeds = 2,       // geodist::EmptySeedsError
+    kCudaError = 3,        // new: device failure (std::runtime_error in the C++ layer)
+    kUnsupported = 4,      // new: shape the kernels cannot take (reported, never a CPU fallback)
+};
+
+struct Status {
+    int code = kOk;
+    std::string msg;
+    bool ok() const { return code == kOk; }
+    static Status Ok() { return {}; }
+    static Status Invalid(std::string m) { return {kInvalidArgument, std::move(m)}; }
+};
+
+// Canonical grid: dims (D, H, W), spacing (sz, sy, sx); 2D grids have D = 1,
+// sz = 1 (ScalarGrid's padding, grid.hpp:69-72 of the reference).
+struct GridDesc {
+    int ndim = 3;
+    int D = 1, H = 1, W = 1;
+    double sz = 1.0, sy = 1.0, sx = 1.0;
+    long long voxels() const { return static_cast<long long>(D) * H * W; }
+};
+
+// Builds a GridDesc from the reference's logical (ndim-long) dims/spacing and
+// validates it exactly like ScalarGrid's constructor (grid.cpp:10-39).
+Status make_grid_desc(int ndim, const int* dims, const double* spacing, GridDesc* out);
+
+struct ScanStats {
+    int rounds = 0;
+    bool converged = true;
+    bool complement_empty = false;
+    double last_change = 0.0;
+    long long kernel_launches = 0;
+};
+
+// Arithmetic mode for 0 < lambda < 1 (Blend): f32 (default, within the
+// 1e-6 abs + 1e-5 rel contract) or the f64 replica of the reference (bit-exact).
+void set_exact_blend(bool on);
+bool exact_blend();
+
+// --- the hot path -----------------------------------------------------------
+// One directional pass (scan_parallel.cpp:298-318).
+Status directional_pass(const GridDesc& g, int B, const float* img, float* dist, int axis,
+                        int orientation, double lambda, cudaStream_t s, ScanStats* st);
+// parallel_scan_inplace (scan_parallel.cpp:320-340): iterations x pass_sequence.
+Status parallel_scan(const GridDesc& g, int B, const float* img, float* dist, double lambda,
+                     int iterations, cudaStream_t s, ScanStats* st);
+// generalized_geodesic (transforms.cpp:143-158).
+Status generalized_geodesic(const GridDesc& g, int B, const float* img, const float* mask,
+                            float* out, double lambda, double nu, int iterations, cudaStream_t s,
+                            ScanStats* st);
+// gsf (transforms.cpp:231-238) = erode(dilate(M, theta), theta).  B must be 1.
+Status gsf(const GridDesc& g, const float* img, const float* mask, float* out, double lambda,
+           double nu, int iterations, double theta, cudaStream_t s, ScanStats* st);
+// scan_to_fixpoint, parallel engine (scan_parallel.cpp:357-397).  B must be 1.
+Status scan_to_fixpoint(const GridDesc& g, const float* img, float* dist, double lambda,
+                        int max_rounds, double tol, cudaStream_t s, ScanStats* st);
+
+// Synthetic benchmark input (tools/main.cpp:67-81) generated on the device.
+Status fill_splitmix(float* out, long long n, unsigned long long seed, cudaStream_t s);
+
+// Number of kernels this library has launched in this process (evidence for
+// bench.py's gpu_launches).
+long long kernel_launch_count();
+
+}  // namespace gdb
