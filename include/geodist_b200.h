@@ -97,7 +97,18 @@ int gd_scan_to_fixpoint(const gd_grid* grid, const float* image, float* dist, do
  * 1e-5 rel of the reference), 1 = f64 replica of the reference (bit-exact). */
 int gd_set_exact_blend(int on);
 
+/* Per-launch CUDA-event profiling, recorded on each launch's own stream.
+ * Classes: 0 sweep (the directional-pass kernel), 1 layout transposes,
+ * 2 soft-mask init, 3 checks/thresholds.  gd_profile_read waits for the
+ * recorded launches and returns accumulated ms, launch counts and algorithmic
+ * bytes (12 B/voxel/pass for the sweep, 8 at lambda = 0) per class. */
+int gd_profile_enable(int on);
+int gd_profile_read(double* ms4, long long* count4, double* bytes4, int reset);
+
 /* Utilities. */
+/* Selects the CUDA device for this thread's subsequent calls (the library
+ * carries its own CUDA runtime state; a caller's cudaSetDevice does not reach it). */
+int gd_set_device(int device);
 const char* gd_last_error(void);
 int gd_version(void);
 long long gd_kernel_launches(void);

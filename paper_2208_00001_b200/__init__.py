@@ -84,6 +84,10 @@ def lib():
         L.gd_last_error.restype = C.c_char_p
         L.gd_kernel_launches.restype = C.c_longlong
         L.gd_fill_splitmix.argtypes = [fp, C.c_longlong, C.c_ulonglong, vp]
+        L.gd_set_device.argtypes = [i]
+        L.gd_profile_enable.argtypes = [i]
+        L.gd_profile_read.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_longlong),
+                                      C.POINTER(C.c_double), i]
         _lib = L
     return _lib
 
@@ -130,6 +134,22 @@ def set_exact_blend(on: bool) -> None:
 
 def kernel_launches() -> int:
     return int(lib().gd_kernel_launches())
+
+
+PROFILE_KINDS = ("sweep", "transpose", "init", "other")
+
+
+def profile_enable(on: bool) -> None:
+    lib().gd_profile_enable(1 if on else 0)
+
+
+def profile_read(reset: bool = True) -> dict:
+    """{kind: (ms, launches, algorithmic_bytes)} accumulated since the last reset."""
+    ms = (C.c_double * 4)()
+    cnt = (C.c_longlong * 4)()
+    by = (C.c_double * 4)()
+    lib().gd_profile_read(ms, cnt, by, 1 if reset else 0)
+    return {k: (ms[i], cnt[i], by[i]) for i, k in enumerate(PROFILE_KINDS)}
 
 
 # ---------------------------------------------------------------- host API
@@ -233,6 +253,15 @@ class device:
     """Same calls on CUDA tensors (torch), enqueued on the current torch stream."""
 
     @staticmethod
+    def set_device(index: int) -> None:
+        _check(lib().gd_set_device(int(index)))
+
+    @staticmethod
+    def _bind(t) -> None:
+        if t.device.index is not None:
+            _check(lib().gd_set_device(int(t.device.index)))
+
+    @staticmethod
     def _stream(stream):
         if stream is not None:
             return C.c_void_p(stream)
@@ -243,6 +272,7 @@ class device:
     def generalized_geodesic(image, soft_mask, out, spacing=None, lam=1.0, nu=1e10,
                              iterations=2, batch=None, stream=None):
         """image/soft_mask/out: contiguous float32 CUDA tensors of shape [B?, (D,) H, W]."""
+        device._bind(image)
         shape = tuple(image.shape)
         if batch:
             g = _grid(shape[1:], spacing)
@@ -258,6 +288,7 @@ class device:
     @staticmethod
     def gsf(image, soft_mask, out, spacing=None, lam=1.0, nu=1e10, iterations=2, theta=0.0,
             stream=None):
+        device._bind(image)
         g = _grid(tuple(image.shape), spacing)
         st = gd_stats()
         _check(lib().gd_gsf(C.byref(g), C.c_void_p(image.data_ptr()),
@@ -268,6 +299,7 @@ class device:
 
     @staticmethod
     def parallel_scan(image, dist, spacing=None, lam=1.0, iterations=2, stream=None):
+        device._bind(image)
         g = _grid(tuple(image.shape), spacing)
         _check(lib().gd_parallel_scan(C.byref(g), C.c_void_p(image.data_ptr()),
                                       C.c_void_p(dist.data_ptr()), lam, iterations,
@@ -275,5 +307,6 @@ class device:
 
     @staticmethod
     def fill_splitmix(out, seed: int, stream=None):
+        device._bind(out)
         _check(lib().gd_fill_splitmix(C.c_void_p(out.data_ptr()), out.numel(),
                                       C.c_ulonglong(seed), device._stream(stream)))

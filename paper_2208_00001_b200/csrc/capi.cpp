@@ -202,6 +202,22 @@ int gd_scan_to_fixpoint(const gd_grid* grid, const float* image, float* dist, do
     return rc;
 }
 
+int gd_set_device(int device) {
+    if (int rc = check_device()) return rc;
+    cudaError_t e = cudaSetDevice(device);
+    return e == cudaSuccess ? GD_OK : cuda_fail(e, "cudaSetDevice");
+}
+
+int gd_profile_enable(int on) {
+    gdb::profile_enable(on != 0);
+    return GD_OK;
+}
+
+int gd_profile_read(double* ms4, long long* count4, double* bytes4, int reset) {
+    gdb::profile_read(ms4, count4, bytes4, reset != 0);
+    return GD_OK;
+}
+
 int gd_fill_splitmix(float* device_out, long long n, unsigned long long seed, void* stream) {
     if (int rc = check_device()) return rc;
     gdb::Status s = gdb::fill_splitmix(device_out, n, seed, static_cast<cudaStream_t>(stream));

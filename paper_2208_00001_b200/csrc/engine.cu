@@ -11,6 +11,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "aux_kernels.cuh"
 #include "engine.cuh"
@@ -23,6 +24,57 @@ namespace {
 
 std::atomic<long long> g_launches{0};
 std::atomic<bool> g_exact_blend{false};
+
+// Optional per-launch CUDA-event timing, recorded on the launching stream
+// (bench.py's roofline numbers).  Off by default.
+struct Profiler {
+    std::mutex mu;
+    bool on = false;
+    struct Rec {
+        cudaEvent_t a, b;
+        int kind;
+        double bytes;
+    };
+    std::vector<Rec> pending;
+    std::vector<cudaEvent_t> pool;
+    double ms[kProfKinds] = {};
+    long long count[kProfKinds] = {};
+    double bytes[kProfKinds] = {};
+    cudaEvent_t get() {
+        if (!pool.empty()) {
+            cudaEvent_t e = pool.back();
+            pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        return e;
+    }
+};
+Profiler g_prof;
+
+// RAII bracket around one launch.
+struct ProfScope {
+    bool active = false;
+    cudaEvent_t a{}, b{};
+    int kind;
+    double bytes;
+    cudaStream_t s;
+    ProfScope(int k, double by, cudaStream_t st) : kind(k), bytes(by), s(st) {
+        std::lock_guard<std::mutex> lk(g_prof.mu);
+        if (!g_prof.on) return;
+        active = true;
+        a = g_prof.get();
+        b = g_prof.get();
+        cudaEventRecord(a, s);
+    }
+    ~ProfScope() {
+        if (!active) return;
+        cudaEventRecord(b, s);
+        std::lock_guard<std::mutex> lk(g_prof.mu);
+        g_prof.pending.push_back({a, b, kind, bytes});
+    }
+};
 
 Status cuda_status(cudaError_t e, const char* what) {
     return {kCudaError, std::string(what) + ": " + cudaGetErrorString(e)};
@@ -151,7 +203,10 @@ Status check_inputs(StreamCtx& sc, const Work& w, const float* mask, bool want_i
     GD_ST(sc.small.ensure(256));
     ImageCheck* dev = sc.small.as<ImageCheck>();
     VolView v = w.canon();
-    GD_CK(launch_image_check(v, want_img ? w.img : nullptr, mask, dev, s));
+    {
+        ProfScope ps(kProfOther, 4.0 * w.B * w.g.voxels() * ((want_img ? 1 : 0) + (mask ? 1 : 0)), s);
+        GD_CK(launch_image_check(v, want_img ? w.img : nullptr, mask, dev, s));
+    }
     ++g_launches;
     ImageCheck h;
     GD_CK(cudaMemcpyAsync(&h, dev, sizeof(h), cudaMemcpyDeviceToHost, s));
@@ -177,6 +232,7 @@ Status ensure_x_layout(StreamCtx& sc, Work& w, bool need_img, cudaStream_t s) {
     if (need_img && !w.iT_ready) {
         GD_ST(sc.iT.ensure(bytes));
         w.iT = sc.iT.as<float>();
+        ProfScope ps(kProfTranspose, 8.0 * w.B * w.g.voxels(), s);
         GD_CK(launch_transpose(w.canon(), w.trans(), w.img, w.iT, true, s));
         ++g_launches;
         w.iT_ready = true;
@@ -283,7 +339,12 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
         p.halo = sc.halo.as<unsigned long long>();
         p.tag_base = sc.tag;
         sc.tag += static_cast<uint32_t>(J + 1);
-        GD_CK(launch_sweep(kind, f64, R, NWU, tm_d, tm_i, p, s));
+        {
+            const double bytes = static_cast<double>(nvol) * g.voxels() * npass *
+                                 (kind == kSpatial ? 8.0 : 12.0);
+            ProfScope ps(kProfSweep, bytes, s);
+            GD_CK(launch_sweep(kind, f64, R, NWU, tm_d, tm_i, p, s));
+        }
         ++g_launches;
         if (st) ++st->kernel_launches;
     }
@@ -293,10 +354,17 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
 Status x_pair(StreamCtx& sc, Work& w, int first_orient, int npass, double lambda, bool f64,
               cudaStream_t s, ScanStats* st) {
     GD_ST(ensure_x_layout(sc, w, lambda != 0.0, s));
-    GD_CK(launch_transpose(w.canon(), w.trans(), w.dist, w.dT, true, s));
+    const double tb = 8.0 * w.B * w.g.voxels();
+    {
+        ProfScope ps(kProfTranspose, tb, s);
+        GD_CK(launch_transpose(w.canon(), w.trans(), w.dist, w.dT, true, s));
+    }
     ++g_launches;
     GD_ST(run_sweep(sc, w, 2, first_orient, npass, lambda, f64, s, st));
-    GD_CK(launch_transpose(w.trans(), w.canon(), w.dT, w.dist, false, s));
+    {
+        ProfScope ps(kProfTranspose, tb, s);
+        GD_CK(launch_transpose(w.trans(), w.canon(), w.dT, w.dist, false, s));
+    }
     ++g_launches;
     return Status::Ok();
 }
@@ -394,7 +462,10 @@ Status generalized_locked(StreamCtx& sc, const GridDesc& g, int B, const float* 
     VolView mv;
     mv.B = B; mv.D = g.D; mv.H = g.H; mv.W = g.W;
     mv.zs = static_cast<long long>(g.H) * g.W; mv.ys = g.W; mv.vol = g.D * mv.zs;
-    GD_CK(launch_init_generalized(mv, w.canon(), mask, w.dist, nu, s));
+    {
+        ProfScope ps(kProfInit, 8.0 * B * g.voxels(), s);
+        GD_CK(launch_init_generalized(mv, w.canon(), mask, w.dist, nu, s));
+    }
     ++g_launches;
     GD_ST(scan_work(sc, w, lambda, iterations, pick_f64(kind, prep), s, st));
     if (padded) GD_ST(unbind(w, out, s));
@@ -428,6 +499,36 @@ Status make_grid_desc(int ndim, const int* dims, const double* spacing, GridDesc
 void set_exact_blend(bool on) { g_exact_blend.store(on); }
 bool exact_blend() { return g_exact_blend.load(); }
 long long kernel_launch_count() { return g_launches.load(); }
+
+void profile_enable(bool on) {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    g_prof.on = on;
+}
+
+void profile_read(double* ms, long long* count, double* bytes, bool reset) {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    for (auto& r : g_prof.pending) {
+        cudaEventSynchronize(r.b);
+        float t = 0.0f;
+        cudaEventElapsedTime(&t, r.a, r.b);
+        g_prof.ms[r.kind] += t;
+        g_prof.count[r.kind] += 1;
+        g_prof.bytes[r.kind] += r.bytes;
+        g_prof.pool.push_back(r.a);
+        g_prof.pool.push_back(r.b);
+    }
+    g_prof.pending.clear();
+    for (int k = 0; k < kProfKinds; ++k) {
+        if (ms) ms[k] = g_prof.ms[k];
+        if (count) count[k] = g_prof.count[k];
+        if (bytes) bytes[k] = g_prof.bytes[k];
+        if (reset) {
+            g_prof.ms[k] = 0.0;
+            g_prof.count[k] = 0;
+            g_prof.bytes[k] = 0.0;
+        }
+    }
+}
 
 Status directional_pass(const GridDesc& g, int B, const float* img, float* dist, int axis,
                         int orientation, double lambda, cudaStream_t s, ScanStats* st) {

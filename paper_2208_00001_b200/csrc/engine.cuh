@@ -77,4 +77,11 @@ Status fill_splitmix(float* out, long long n, unsigned long long seed, cudaStrea
 // bench.py's gpu_launches).
 long long kernel_launch_count();
 
+// Per-launch CUDA-event profiling by kernel class (on the launching stream).
+enum ProfKind : int { kProfSweep = 0, kProfTranspose = 1, kProfInit = 2, kProfOther = 3, kProfKinds = 4 };
+void profile_enable(bool on);
+// Collects finished launches (synchronising on their end events) and returns
+// accumulated milliseconds, launch counts and algorithmic bytes per class.
+void profile_read(double* ms, long long* count, double* bytes, bool reset);
+
 }  // namespace gdb
