@@ -270,25 +270,38 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
     if (ns < 2) return Status::Ok();  // scan_parallel.cpp:308-310
     const int kind = cost_kind(lambda);
     if (kind == kSpatial) ibase = dbase;  // intensities never read; any valid map will do
-    const int R = nu == 1 ? 1 : 4;
-    const int NWU = nu == 1 ? 1 : 8;
-    const int TU = R * NWU;
-    const int ntu = (nu + TU - 1) / TU;
-    const int ntv = (nv + kTV - 1) / kTV;
-    const long long per_vol = static_cast<long long>(ntu) * ntv;
-    const int maxc = sweep_max_coresident(R, NWU, kind, f64);
-    if (maxc <= 0) return {kCudaError, "sweep kernel cannot be resident on this device"};
-    if (per_vol > maxc)
+    const int nwv = (nv + kWV - 1) / kWV;
+    if (nwv > kMaxWarps)
+        return {kUnsupported, "plane width " + std::to_string(nv) + " exceeds " +
+                                  std::to_string(kMaxWarps * kWV) + " columns"};
+    // Rows per strip: the smallest R whose strips are all co-resident, preferring
+    // R = 4 (enough rows to hide the halo latency behind the strip interior).
+    int R = 0, maxc = 0;
+    long long per_vol = 0;
+    const int pref[] = {4, 8, 2, 1};
+    for (int cand : pref) {
+        if (nu == 1 && cand != 1) continue;
+        if (nwv > 4 && cand == 8) continue;
+        const int mc = sweep_max_coresident(cand, nwv, kind, f64);
+        const long long pv = (nu + cand - 1) / cand;
+        if (mc > 0 && pv <= mc) {
+            R = cand;
+            maxc = mc;
+            per_vol = pv;
+            break;
+        }
+    }
+    if (R == 0)
         return {kUnsupported, "plane of " + std::to_string(nu) + "x" + std::to_string(nv) +
-                                  " needs " + std::to_string(per_vol) + " co-resident tiles (max " +
-                                  std::to_string(maxc) + ")"};
+                                  " has more row strips than co-resident CTAs"};
+    const int ntu = static_cast<int>(per_vol);
     const int group = static_cast<int>(std::min<long long>(w.B, maxc / per_vol));
-    const int HALO_N = 2 * kTV + 2 * TU;
+    const long long strip_words = 2ll * 2 * nwv * kWV;
     const int J = npass * (ns - 1);
 
     SweepParams p{};
     p.ss = ss; p.su = su; p.vol_stride = vol;
-    p.ns = ns; p.nu = nu; p.nv = nv; p.ntu = ntu; p.ntv = ntv;
+    p.ns = ns; p.nu = nu; p.nv = nv; p.ntu = ntu; p.nwv = nwv;
     p.tma_sweep_dim = sweep_dim;
     p.first_orient = first_orient;
     p.npass = npass;
@@ -310,11 +323,11 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
 
     uint32_t box_d[4], box_i[4];
     if (sweep_dim == 2) {
-        box_d[0] = kTV; box_d[1] = TU; box_d[2] = 1; box_d[3] = 1;
-        box_i[0] = kIW; box_i[1] = TU + 2; box_i[2] = 1; box_i[3] = 1;
+        box_d[0] = kWV; box_d[1] = R; box_d[2] = 1; box_d[3] = 1;
+        box_i[0] = kIW; box_i[1] = R + 2; box_i[2] = 1; box_i[3] = 1;
     } else {
-        box_d[0] = kTV; box_d[1] = 1; box_d[2] = TU; box_d[3] = 1;
-        box_i[0] = kIW; box_i[1] = 1; box_i[2] = TU + 2; box_i[3] = 1;
+        box_d[0] = kWV; box_d[1] = 1; box_d[2] = R; box_d[3] = 1;
+        box_i[0] = kIW; box_i[1] = 1; box_i[2] = R + 2; box_i[3] = 1;
     }
 
     for (int b0 = 0; b0 < w.B; b0 += group) {
@@ -323,7 +336,7 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
         CUtensorMap tm_d, tm_i;
         GD_ST(make_map(&tm_d, dbase + b0 * vol, dims, strides, box_d));
         GD_ST(make_map(&tm_i, ibase + b0 * vol, dims, strides, box_i));
-        const size_t words = static_cast<size_t>(nvol) * per_vol * 2 * HALO_N;
+        const size_t words = static_cast<size_t>(nvol) * per_vol * strip_words;
         GD_ST(sc.halo.ensure(words * 8));
         if (sc.halo_bytes_zeroed < sc.halo.n) {
             GD_CK(cudaMemsetAsync(sc.halo.p, 0, sc.halo.n, s));
@@ -343,7 +356,7 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
             const double bytes = static_cast<double>(nvol) * g.voxels() * npass *
                                  (kind == kSpatial ? 8.0 : 12.0);
             ProfScope ps(kProfSweep, bytes, s);
-            GD_CK(launch_sweep(kind, f64, R, NWU, tm_d, tm_i, p, s));
+            GD_CK(launch_sweep(kind, f64, R, tm_d, tm_i, p, s));
         }
         ++g_launches;
         if (st) ++st->kernel_launches;

@@ -70,6 +70,21 @@ __device__ __forceinline__ unsigned long long ld_tagged(const unsigned long long
     return w;
 }
 
+// Two adjacent words in one 16-byte access; each 8-byte element is still
+// single-copy atomic (vector accesses behave as per-element scalar accesses).
+__device__ __forceinline__ void st_tagged2(unsigned long long* p, float v0, float v1, uint32_t tag) {
+    const unsigned long long w0 = (static_cast<unsigned long long>(tag) << 32) | __float_as_uint(v0);
+    const unsigned long long w1 = (static_cast<unsigned long long>(tag) << 32) | __float_as_uint(v1);
+    asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(w0), "l"(w1)
+                 : "memory");
+}
+
+__device__ __forceinline__ void ld_tagged2(const unsigned long long* p, unsigned long long& w0,
+                                           unsigned long long& w1) {
+    asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(p)
+                 : "memory");
+}
+
 __device__ __forceinline__ uint32_t tag_of(unsigned long long w) {
     return static_cast<uint32_t>(w >> 32);
 }

@@ -8,23 +8,27 @@
 //
 // Geometry.  One launch sweeps axis "s" of a batch of volumes, optionally
 // forward then backward.  The plane perpendicular to s has a slow axis u and a
-// contiguous axis v.  Each CTA owns a TU x 64 tile of that plane (NWU warps
-// stacked along u, R rows per warp, 2 consecutive v columns per lane) for the
-// whole sweep and keeps the previous plane's new distances and intensities in
-// registers.  In-plane neighbours come from warp shuffles (v +- 1), own
-// registers (u +- 1 inside a warp) and shared memory (rows at warp borders).
+// contiguous axis v.  Each CTA owns a full-width strip of R rows of that plane
+// (u in [u0, u0+R), every v) for the whole sweep: NWV warps side by side, each
+// lane holding C = 4 consecutive columns of all R rows in registers.  Strips
+// only have neighbours above and below, so there is no column halo at all:
+// v +- 1 comes from warp shuffles, warp-edge columns from the neighbour warp's
+// previous-step values in shared memory, u +- 1 inside the strip from the
+// thread's own registers.
 //
 // Staging.  An NST-deep ring of TMA boxes brings each upcoming plane's old
-// distances (TU x 64) and intensities with a 1-voxel halo ((TU+2) x 72) into
-// shared memory, completion tracked by one mbarrier per slot.
+// distances (R x 128 per warp) and intensities with a row halo and a 4-column
+// margin ((R+2) x 136 per warp) into shared memory; one mbarrier per slot, each
+// warp arms it with its own boxes.
 //
-// Halo hand-off.  The 1-voxel ring of the previous plane owned by neighbour
-// tiles arrives through global memory as tagged 64-bit words {f32 value, u32
-// tag}: single-copy-atomic relaxed stores by the owner, relaxed polling loads
-// by the reader until the tag equals the expected step.  No fences, no flags,
-// no grid barrier.  The loads are issued before the interior of the plane is
-// relaxed, so their latency hides behind that work; only the tile's border
-// voxels wait for them.
+// Halo hand-off.  The previous plane's row above and row below the strip come
+// from the neighbouring strips through global memory as tagged 64-bit words
+// {f32 value, u32 tag}: single-copy-atomic relaxed stores by the owner, relaxed
+// loads by the reader until the tag equals the expected step.  Each lane loads
+// exactly the 6 words (v-1 .. v+4) it needs, so the hand-off needs no shared
+// memory and no barrier.  The loads are issued at the top of the step and only
+// checked after the strip interior has been relaxed, which hides their latency
+// (~750 cycles per hop measured, tools/micro/halo_latency.cu).
 //
 // Arithmetic (bit-exact contract with the reference, which relaxes in f64 and
 // stores f32 once per voxel per pass): rounding to f32 is monotone, so
@@ -34,8 +38,8 @@
 //     first (exact: monotone), then one f64 add per class and one rounding.
 //   * Intensity (lambda == 1): f32 `d_q + |I_p - I_q|` is exactly the
 //     reference's f32(f64(d_q) + |di|) whenever I_p - I_q is exact in f32; the
-//     host checks that per image (image_diff_exact) and otherwise selects the
-//     f64 path.
+//     host checks that per image (image_check_kernel) and otherwise selects the
+//     f64 path.  Column pairs go through packed FADD2 (sm_100 f32x2).
 //   * Blend: f32 arithmetic within the 1e-6 abs + 1e-5 rel tolerance; the f64
 //     path (sqrt(fma(lambda*di, di, c0)) exactly as compiled in the reference)
 //     when exact mode is requested.
@@ -50,22 +54,25 @@ namespace gdb {
 
 enum CostKind : int { kSpatial = 0, kIntensity = 1, kBlend = 2 };
 
-constexpr int kTV = 64;   // tile width along v (2 columns per lane)
-constexpr int kIW = 72;   // intensity box width: v0-4 .. v0+67 (16-byte aligned)
+constexpr int kC = 4;            // columns per lane
+constexpr int kWV = 32 * kC;     // columns per warp (128)
+constexpr int kIW = kWV + 8;     // intensity box width per warp: v0w-4 .. v0w+131
+constexpr int kMaxWarps = 16;    // strip width limit: 16 * 128 = 2048 columns
 
 struct SweepParams {
     float* dist;              // volume 0 of this launch
     long long vol_stride;     // elements between volumes
     long long ss, su;         // element strides of the sweep axis and of u (v stride = 1)
     int ns, nu, nv;           // extents
-    int ntu, ntv;             // tiles per volume
+    int ntu;                  // strips per volume
     int nvol;                 // volumes in this launch
+    int nwv;                  // warps across the strip
     int tma_sweep_dim;        // tensor-map dim carrying s (2: z-form, 1: y-form)
     int first_orient;         // +1 / -1
     int npass;                // 1 or 2 (second pass runs the opposite orientation)
     int fence_turn;           // emit fence.proxy.async on forward stores (npass == 2)
     uint32_t tag_base;
-    unsigned long long* halo; // tagged halo words
+    unsigned long long* halo; // tagged halo words: [strip][parity][TOP|BOT][nwv*128]
     // Neighbour coefficients indexed (du+1)*3 + (dv+1).
     double rho[9];
     double c0[9];
@@ -74,14 +81,10 @@ struct SweepParams {
     float lambda_f;
 };
 
-struct SweepTileConfig {
-    int R, NWU, NST;
-};
-
-// Host-side launch (defined in sweep.cu).
-cudaError_t launch_sweep(int kind, bool f64, int R, int NWU, const CUtensorMap& tm_d,
+// Host-side launch (defined in sweep.cu).  R = rows per strip.
+cudaError_t launch_sweep(int kind, bool f64, int R, const CUtensorMap& tm_d,
                          const CUtensorMap& tm_i, const SweepParams& p, cudaStream_t stream);
-size_t sweep_smem_bytes(int R, int NWU);
-int sweep_max_coresident(int R, int NWU, int kind, bool f64);
+size_t sweep_smem_bytes(int R, int nwv);
+int sweep_max_coresident(int R, int nwv, int kind, bool f64);
 
 }  // namespace gdb
