@@ -104,6 +104,9 @@ int gd_set_exact_blend(int on);
  * bytes (12 B/voxel/pass for the sweep, 8 at lambda = 0) per class. */
 int gd_profile_enable(int on);
 int gd_profile_read(double* ms4, long long* count4, double* bytes4, int reset);
+/* Per-launch (class, ms) in launch order for the launches collected by the last
+ * gd_profile_read (call it with reset = 0 first); returns the number logged. */
+int gd_profile_log(int* kinds, float* ms, int max);
 
 /* Utilities. */
 /* Selects the CUDA device for this thread's subsequent calls (the library

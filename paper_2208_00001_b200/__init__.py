@@ -152,6 +152,14 @@ def profile_read(reset: bool = True) -> dict:
     return {k: (ms[i], cnt[i], by[i]) for i, k in enumerate(PROFILE_KINDS)}
 
 
+def profile_log(max_entries: int = 4096):
+    """[(kind, ms)] per launch for the launches gathered by profile_read(reset=False)."""
+    kinds = (C.c_int * max_entries)()
+    ms = (C.c_float * max_entries)()
+    n = lib().gd_profile_log(kinds, ms, max_entries)
+    return [(PROFILE_KINDS[kinds[i]], ms[i]) for i in range(min(n, max_entries))]
+
+
 # ---------------------------------------------------------------- host API
 def generalized_geodesic(image, soft_mask, spacing=None, lam=1.0, nu=1e10, iterations=2,
                          stats: dict | None = None) -> np.ndarray:

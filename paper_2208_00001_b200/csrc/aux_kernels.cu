@@ -5,6 +5,7 @@
 // where the layout allows, grid sized as a multiple of the SM count.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "aux_kernels.cuh"
@@ -48,7 +49,7 @@ template <bool FWD>
 __global__ void transpose_kernel(VolView src_v, VolView dst_v, const float* src, float* dst) {
     __shared__ float tile[32][33];
     const int D = src_v.D, H = src_v.H, W = src_v.W;
-    const int bz = blockIdx.z;
+    for (int bz = blockIdx.z; bz < D * src_v.B; bz += gridDim.z) {
     const int z = bz % D, b = bz / D;
     const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
     const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
@@ -78,6 +79,8 @@ __global__ void transpose_kernel(VolView src_v, VolView dst_v, const float* src,
             if (y < H && x < W)
                 dst[b * dst_v.vol + z * dst_v.zs + static_cast<long long>(y) * dst_v.ys + x] = tile[tx][k];
         }
+    }
+    __syncthreads();
     }
 }
 
@@ -233,7 +236,7 @@ cudaError_t launch_transpose(const VolView& src_v, const VolView& dst_v, const f
     // src_v / dst_v carry the logical (D, H, W) of the [z][y][x] volume in both
     // directions; zs/ys/vol are the respective layouts' strides.
     const VolView& lv = forward ? src_v : dst_v;
-    dim3 grid((lv.W + 31) / 32, (lv.H + 31) / 32, lv.D * lv.B);
+    dim3 grid((lv.W + 31) / 32, (lv.H + 31) / 32, std::min(lv.D * lv.B, 65535));
     dim3 block(32, 8);
     VolView a = src_v, b = dst_v;
     a.D = b.D = lv.D;

@@ -218,6 +218,8 @@ int gd_profile_read(double* ms4, long long* count4, double* bytes4, int reset) {
     return GD_OK;
 }
 
+int gd_profile_log(int* kinds, float* ms, int max) { return gdb::profile_log(kinds, ms, max); }
+
 int gd_fill_splitmix(float* device_out, long long n, unsigned long long seed, void* stream) {
     if (int rc = check_device()) return rc;
     gdb::Status s = gdb::fill_splitmix(device_out, n, seed, static_cast<cudaStream_t>(stream));

@@ -4,6 +4,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdint>
@@ -38,6 +39,7 @@ struct Profiler {
     std::vector<Rec> pending;
     std::vector<cudaEvent_t> pool;
     double ms[kProfKinds] = {};
+    std::vector<std::pair<int, float>> log;  // (kind, ms) per launch, in launch order
     long long count[kProfKinds] = {};
     double bytes[kProfKinds] = {};
     cudaEvent_t get() {
@@ -525,6 +527,7 @@ void profile_read(double* ms, long long* count, double* bytes, bool reset) {
         float t = 0.0f;
         cudaEventElapsedTime(&t, r.a, r.b);
         g_prof.ms[r.kind] += t;
+        g_prof.log.emplace_back(r.kind, t);
         g_prof.count[r.kind] += 1;
         g_prof.bytes[r.kind] += r.bytes;
         g_prof.pool.push_back(r.a);
@@ -536,6 +539,7 @@ void profile_read(double* ms, long long* count, double* bytes, bool reset) {
         if (count) count[k] = g_prof.count[k];
         if (bytes) bytes[k] = g_prof.bytes[k];
         if (reset) {
+            if (k == 0) g_prof.log.clear();
             g_prof.ms[k] = 0.0;
             g_prof.count[k] = 0;
             g_prof.bytes[k] = 0.0;
@@ -682,6 +686,16 @@ Status fill_splitmix(float* out, long long n, unsigned long long seed, cudaStrea
     GD_CK(launch_splitmix(out, n, seed, s));
     ++g_launches;
     return Status::Ok();
+}
+
+int profile_log(int* kinds, float* ms, int max) {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    const int n = static_cast<int>(std::min<size_t>(g_prof.log.size(), static_cast<size_t>(max)));
+    for (int i = 0; i < n; ++i) {
+        kinds[i] = g_prof.log[i].first;
+        ms[i] = g_prof.log[i].second;
+    }
+    return static_cast<int>(g_prof.log.size());
 }
 
 }  // namespace gdb

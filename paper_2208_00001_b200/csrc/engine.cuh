@@ -83,5 +83,8 @@ void profile_enable(bool on);
 // Collects finished launches (synchronising on their end events) and returns
 // accumulated milliseconds, launch counts and algorithmic bytes per class.
 void profile_read(double* ms, long long* count, double* bytes, bool reset);
+// Per-launch (kind, ms) of the launches collected by the last profile_read
+// (before its reset); returns the total number logged.
+int profile_log(int* kinds, float* ms, int max);
 
 }  // namespace gdb

@@ -97,13 +97,18 @@ struct Acc<kSpatial, F64> {
     }
 };
 
+// FADD2 packing of column pairs: off — ptxas cannot fold |d| into the packed
+// add and the odd-aligned pairs cost register moves (measured: 86 vs 68
+// instructions per voxel); the scalar FADD with an |operand| is cheaper.
+constexpr bool kPackedIntensity = false;
+
 // The 3-column windows of one previous-plane row for a lane's 4 columns:
 // pw/iw[0] = column v-1, [1..4] = own columns, [5] = column v+4.
 template <int KIND, bool F64>
 __device__ __forceinline__ void relax_row(Acc<KIND, F64> (&acc)[kC], const float (&pw)[6],
                                           const float (&iw)[6], const float (&ip)[kC], int du,
                                           const SweepParams& p) {
-    if constexpr (KIND == kIntensity && !F64) {
+    if constexpr (KIND == kIntensity && !F64 && kPackedIntensity) {
         // Packed column pairs: two FADD2 per candidate pair instead of four FADD.
 #pragma unroll
         for (int q = 0; q < kC / 2; ++q) {
@@ -130,14 +135,16 @@ __device__ __forceinline__ void relax_row(Acc<KIND, F64> (&acc)[kC], const float
     }
 }
 
-template <int R, int NST>
+template <int RW, int NWU, int NST>
 struct Layout {
-    static constexpr int DBOX = R * kWV;                          // floats per warp box
+    static constexpr int R = RW * NWU;                            // rows per strip
+    static constexpr int DBOX = R * kWV;                          // floats per column-block box
     static constexpr int IBOX = ((R + 2) * kIW + 31) / 32 * 32;   // 128-B aligned slot stride
     static constexpr int IBYTES = (R + 2) * kIW * 4;
     static size_t smem_bytes(int nwv) {
-        return static_cast<size_t>(NST) * nwv * (DBOX + IBOX) * 4  // TMA ring
-               + static_cast<size_t>(2) * nwv * 2 * R * 4          // warp-edge columns
+        return static_cast<size_t>(NST) * nwv * (DBOX + IBOX) * 4     // TMA ring
+               + static_cast<size_t>(2) * NWU * 2 * nwv * kWV * 4     // warp-row boundary rows
+               + static_cast<size_t>(2) * NWU * nwv * 2 * RW * 4      // warp-edge columns
                + NST * 8 + 128;
     }
 };
@@ -151,35 +158,52 @@ __device__ __forceinline__ void load_halo_row(const unsigned long long* q, bool 
     h[5] = has_right ? ld_tagged(q + 4) : 0ull;
 }
 
-template <int KIND, bool F64, int R, int NST, int MW>
-__global__ void __launch_bounds__(MW * 32, 1)
+// A previous-plane row window for this lane: own 4 columns from `c4`, the
+// neighbours v-1 / v+4 from the adjacent lanes, and at the warp edges from
+// `edge_l` / `edge_r` (column 128wv-1 / 128wv+128).
+__device__ __forceinline__ void make_window(const float (&c4)[kC], float edge_l, float edge_r,
+                                            int lane, float (&win)[6]) {
+#pragma unroll
+    for (int c = 0; c < kC; ++c) win[c + 1] = c4[c];
+    const float up = __shfl_up_sync(kFull, c4[kC - 1], 1);
+    const float dn = __shfl_down_sync(kFull, c4[0], 1);
+    win[0] = lane == 0 ? edge_l : up;
+    win[5] = lane == 31 ? edge_r : dn;
+}
+
+template <int KIND, bool F64, int RW, int NWU, int NST, int MW>
+__global__ void __launch_bounds__(MW * NWU * 32, 1)
     sweep_kernel(const __grid_constant__ CUtensorMap tm_d, const __grid_constant__ CUtensorMap tm_i,
                  const __grid_constant__ SweepParams p) {
-    using L = Layout<R, NST>;
-    constexpr int DBOX = L::DBOX, IBOX = L::IBOX;
+    using L = Layout<RW, NWU, NST>;
+    constexpr int R = L::R, DBOX = L::DBOX, IBOX = L::IBOX;
     // Spatial (lambda == 0) never reads intensities: only the distance box moves.
     constexpr uint32_t TXW =
         static_cast<uint32_t>(KIND == kSpatial ? DBOX * 4 : DBOX * 4 + L::IBYTES);
+    constexpr bool kI = KIND != kSpatial;
 
     const int nwv = p.nwv;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int wu = w / nwv, wv = w - wu * nwv;   // warp row / warp column
+    const int r0 = wu * RW;                      // first strip row of this warp
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    float* sd = reinterpret_cast<float*>(smem_raw);   // [NST][nwv][R][128]
-    float* si = sd + NST * nwv * DBOX;                 // [NST][nwv][R+2][136]
-    float* edge = si + NST * nwv * IBOX;               // [2][nwv][2][R]  (left col, right col)
-    uint64_t* bar = reinterpret_cast<uint64_t*>(edge + 2 * nwv * 2 * R);
+    float* sd = reinterpret_cast<float*>(smem_raw);     // [NST][nwv][R][128]
+    float* si = sd + NST * nwv * DBOX;                   // [NST][nwv][R+2][136]
+    float* rows = si + NST * nwv * IBOX;                 // [2][NWU][first|last][nwv*128]
+    float* edge = rows + 2 * NWU * 2 * nwv * kWV;        // [2][NWU][nwv][left|right][RW]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(edge + 2 * NWU * nwv * 2 * RW);
 
     const int g = blockIdx.x;
     const int b = g / p.ntu;
     const int tu = g - b * p.ntu;
     const int u0 = tu * R;
-    const int v0w = w * kWV;              // first column of this warp
-    const int vl = v0w + kC * lane;        // first column of this lane
+    const int v0w = wv * kWV;              // first column of this warp
+    const int vl = v0w + kC * lane;         // first column of this lane
     const int n1 = p.ns - 1;
     const int J = p.npass * n1;
     const float INF = finf();
-    const int VW = nwv * kWV;             // halo row length (words)
+    const int VW = nwv * kWV;              // strip width in words / floats
 
     auto plane_of = [&](int j) -> int {
         if (j <= n1) return p.first_orient > 0 ? j : n1 - j;
@@ -191,14 +215,13 @@ __global__ void __launch_bounds__(MW * 32, 1)
         for (int s = 0; s < NST; ++s) mbar_init(&bar[s], nwv);
         fence_mbar_init();
     }
-    if (lane == 0) {
+    const bool producer = wu == 0 && lane == 0;  // streams column block wv
+    if (producer) {
         tma_prefetch_desc(&tm_d);
-        if (KIND != kSpatial) tma_prefetch_desc(&tm_i);
+        if (kI) tma_prefetch_desc(&tm_i);
     }
     __syncthreads();
 
-    // Each warp's lane 0 streams its own column block; the slot's mbarrier
-    // completes when all nwv warps' boxes have landed.
     int issued = 0;
     auto issue = [&](int t) {
         // Slot j % NST is free once step j-NST+1 (which reads it as the
@@ -211,46 +234,46 @@ __global__ void __launch_bounds__(MW * 32, 1)
             const int slot = j % NST;
             const int s = plane_of(j);
             mbar_arrive_expect_tx(&bar[slot], TXW);
-            float* dd = sd + (slot * nwv + w) * DBOX;
-            float* di = si + (slot * nwv + w) * IBOX;
+            float* dd = sd + (slot * nwv + wv) * DBOX;
+            float* di = si + (slot * nwv + wv) * IBOX;
             if (p.tma_sweep_dim == 2) {
                 tma_load_4d(dd, &tm_d, &bar[slot], v0w, u0, s, b);
-                if (KIND != kSpatial) tma_load_4d(di, &tm_i, &bar[slot], v0w - 4, u0 - 1, s, b);
+                if (kI) tma_load_4d(di, &tm_i, &bar[slot], v0w - 4, u0 - 1, s, b);
             } else {
                 tma_load_4d(dd, &tm_d, &bar[slot], v0w, s, u0, b);
-                if (KIND != kSpatial) tma_load_4d(di, &tm_i, &bar[slot], v0w - 4, s, u0 - 1, b);
+                if (kI) tma_load_4d(di, &tm_i, &bar[slot], v0w - 4, s, u0 - 1, b);
             }
             ++issued;
         }
     };
 
     // Tagged halo rows: the strip above publishes its BOT row, the one below its TOP row.
-    const bool has_up = tu > 0, has_dn = tu + 1 < p.ntu;
+    const bool top_warp = wu == 0, bot_warp = wu == NWU - 1;
+    const bool has_up = tu > 0 && top_warp, has_dn = tu + 1 < p.ntu && bot_warp;
     const long long strip_words = 2ll * 2 * VW;  // per strip: 2 parities x {TOP, BOT}
     const long long strip0 = static_cast<long long>(b) * p.ntu;
     const unsigned long long* up_base = p.halo + (strip0 + tu - 1) * strip_words + VW + vl;
     const unsigned long long* dn_base = p.halo + (strip0 + tu + 1) * strip_words + vl;
     unsigned long long* self_base = p.halo + static_cast<long long>(g) * strip_words + vl;
+    const bool pub_top = tu > 0 && top_warp, pub_bot = tu + 1 < p.ntu && bot_warp;
     const bool has_left = vl > 0, has_right = vl + kC < p.nv;  // lane-level edge words
 
-    // Validity of this thread's voxels (rows beyond nu / columns beyond nv are +inf).
-    bool rowv[R], colv[kC];
+    bool rowv[RW], colv[kC];
 #pragma unroll
-    for (int r = 0; r < R; ++r) rowv[r] = (u0 + r) < p.nu;
+    for (int r = 0; r < RW; ++r) rowv[r] = (u0 + r0 + r) < p.nu;
 #pragma unroll
     for (int c = 0; c < kC; ++c) colv[c] = (vl + c) < p.nv;
 
-    float P[R][kC], IP[R][kC];  // previous plane: new distances / intensities of own voxels
+    float P[RW][kC], IP[RW][kC];  // previous plane: new distances / intensities of own voxels
 
     for (int j = 0; j <= J; ++j) {
-        __syncthreads();  // step j-1 complete: edge columns visible, slot (j-2)%NST free
-        if (lane == 0) issue(j);
+        __syncthreads();  // step j-1 complete: boundary rows/edges visible, slot (j-2)%NST free
+        if (producer) issue(j);
 
         const int par = (j - 1) & 1;
         const long long hoff = par * 2ll * VW;
         const uint32_t want = p.tag_base + static_cast<uint32_t>(j - 1);
-        // halo words for the previous plane: [0] = v-1, [1..4] own, [5] = v+4
-        unsigned long long hu[6], hd[6];
+        unsigned long long hu[6], hd[6];  // [0] = v-1, [1..4] own, [5] = v+4
         if (j > 0) {
             if (has_up) load_halo_row(up_base + hoff, has_left, has_right, hu);
             if (has_dn) load_halo_row(dn_base + hoff, has_left, has_right, hd);
@@ -258,16 +281,16 @@ __global__ void __launch_bounds__(MW * 32, 1)
 
         const int slot = j % NST;
         mbar_wait(&bar[slot], static_cast<uint32_t>((j / NST) & 1));
-        const float* sdc = sd + (slot * nwv + w) * DBOX;
-        const float* sic = si + (slot * nwv + w) * IBOX;
-        float dold[R][kC], ic[R][kC];
+        const float* sdc = sd + (slot * nwv + wv) * DBOX;
+        const float* sic = si + (slot * nwv + wv) * IBOX;
+        float dold[RW][kC], ic[RW][kC];
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const float4 d4 = *reinterpret_cast<const float4*>(sdc + r * kWV + kC * lane);
+        for (int r = 0; r < RW; ++r) {
+            const float4 d4 = *reinterpret_cast<const float4*>(sdc + (r0 + r) * kWV + kC * lane);
             dold[r][0] = d4.x; dold[r][1] = d4.y; dold[r][2] = d4.z; dold[r][3] = d4.w;
-            if (KIND != kSpatial) {
-                const float4 i4 =
-                    *reinterpret_cast<const float4*>(sic + (r + 1) * kIW + 4 + kC * lane);
+            if (kI) {
+                const float4 i4 = *reinterpret_cast<const float4*>(sic + (r0 + r + 1) * kIW + 4 +
+                                                                   kC * lane);
                 ic[r][0] = i4.x; ic[r][1] = i4.y; ic[r][2] = i4.z; ic[r][3] = i4.w;
             } else {
 #pragma unroll
@@ -275,126 +298,155 @@ __global__ void __launch_bounds__(MW * 32, 1)
             }
         }
 
-        float N[R][kC];
+        float N[RW][kC];
         if (j == 0) {
 #pragma unroll
-            for (int r = 0; r < R; ++r)
+            for (int r = 0; r < RW; ++r)
 #pragma unroll
                 for (int c = 0; c < kC; ++c) N[r][c] = (rowv[r] && colv[c]) ? dold[r][c] : INF;
         } else {
-            const float* sip = si + (((j - 1) % NST) * nwv + w) * IBOX;  // previous plane's I box
-            const float* edge_prev = edge + par * nwv * 2 * R;
-            Acc<KIND, F64> acc[R][kC];
+            const float* sip = si + (((j - 1) % NST) * nwv + wv) * IBOX;  // previous plane's I box
+            const float* rows_prev = rows + par * NWU * 2 * VW;
+            const float* edge_prev = edge + par * NWU * nwv * 2 * RW;
+            Acc<KIND, F64> acc[RW][kC];
 #pragma unroll
-            for (int r = 0; r < R; ++r)
+            for (int r = 0; r < RW; ++r)
 #pragma unroll
                 for (int c = 0; c < kC; ++c) acc[r][c].init(dold[r][c]);
 
-            // ---- phase A: previous-plane rows inside the strip --------------
-#pragma unroll
-            for (int k = 0; k < R; ++k) {
-                float pw[6], iw[6];
-#pragma unroll
-                for (int c = 0; c < kC; ++c) {
-                    pw[c + 1] = P[k][c];
-                    iw[c + 1] = IP[k][c];
-                }
-                // v-1: lane-1's last column; at the warp edge, the left warp's right column
-                const float eL = w > 0 ? edge_prev[((w - 1) * 2 + 1) * R + k] : INF;
-                const float eR = w + 1 < nwv ? edge_prev[((w + 1) * 2 + 0) * R + k] : INF;
-                pw[0] = __shfl_up_sync(kFull, P[k][kC - 1], 1);
-                pw[5] = __shfl_down_sync(kFull, P[k][0], 1);
-                if (lane == 0) pw[0] = eL;
-                if (lane == 31) pw[5] = eR;
-                if (KIND != kSpatial) {
-                    iw[0] = __shfl_up_sync(kFull, IP[k][kC - 1], 1);
-                    iw[5] = __shfl_down_sync(kFull, IP[k][0], 1);
-                    if (lane == 0) iw[0] = sip[(k + 1) * kIW + 3];
-                    if (lane == 31) iw[5] = sip[(k + 1) * kIW + 4 + kWV];
-                } else {
-                    iw[0] = iw[5] = 0.0f;
-                }
-                // prev row k feeds output rows k-1 (du=+1), k (du=0), k+1 (du=-1)
-                if (k - 1 >= 0) relax_row<KIND, F64>(acc[k - 1], pw, iw, ic[k - 1], +1, p);
-                relax_row<KIND, F64>(acc[k], pw, iw, ic[k], 0, p);
-                if (k + 1 < R) relax_row<KIND, F64>(acc[k + 1], pw, iw, ic[k + 1], -1, p);
-            }
-
-            // ---- phase B: the rows above / below the strip (tagged halo) -----
-            if (has_up || has_dn) {
-                long long spins = 0;
-                while (true) {
-                    bool ok = true;
-#pragma unroll
-                    for (int i = 0; i < 6; ++i) {
-                        const bool need = (i > 0 && i < 5) || (i == 0 ? has_left : has_right);
-                        if (has_up && need && tag_of(hu[i]) != want) {
-                            hu[i] = ld_tagged(up_base + hoff + i - 1);
-                            ok = false;
-                        }
-                        if (has_dn && need && tag_of(hd[i]) != want) {
-                            hd[i] = ld_tagged(dn_base + hoff + i - 1);
-                            ok = false;
-                        }
-                    }
-                    if (ok) break;
-                    if (++spins > kSpinLimit) __trap();
-                }
-            }
-#pragma unroll
-            for (int side = 0; side < 2; ++side) {
-                // side 0: row u0-1 -> output row 0 (du = -1); side 1: row u0+R -> row R-1 (du = +1)
-                const bool has = side == 0 ? has_up : has_dn;
-                float pw[6], iw[6];
-#pragma unroll
-                for (int i = 0; i < 6; ++i) {
-                    const bool need = (i > 0 && i < 5) || (i == 0 ? has_left : has_right);
-                    pw[i] = (has && need) ? val_of(side == 0 ? hu[i] : hd[i]) : INF;
-                }
-                if (KIND != kSpatial) {
-                    const float* rowp = sip + (side == 0 ? 0 : (R + 1) * kIW);
-                    const float4 i4 = *reinterpret_cast<const float4*>(rowp + 4 + kC * lane);
-                    iw[1] = i4.x; iw[2] = i4.y; iw[3] = i4.z; iw[4] = i4.w;
-                    iw[0] = __shfl_up_sync(kFull, iw[4], 1);
-                    iw[5] = __shfl_down_sync(kFull, iw[1], 1);
-                    if (lane == 0) iw[0] = rowp[3];
-                    if (lane == 31) iw[5] = rowp[4 + kWV];
+            // Intensity window of previous-plane strip row `sr` (box row sr+1).
+            auto i_window = [&](int sr, float (&iw)[6]) {
+                if (kI) {
+                    const float* rp = sip + (sr + 1) * kIW;
+                    const float4 i4 = *reinterpret_cast<const float4*>(rp + 4 + kC * lane);
+                    const float c4[kC] = {i4.x, i4.y, i4.z, i4.w};
+                    make_window(c4, rp[3], rp[4 + kWV], lane, iw);
                 } else {
 #pragma unroll
                     for (int i = 0; i < 6; ++i) iw[i] = 0.0f;
                 }
-                if (side == 0)
+            };
+
+            // ---- phase A: previous-plane rows held inside the CTA ------------
+#pragma unroll
+            for (int k = 0; k < RW; ++k) {
+                float pw[6], iw[6];
+                const float eL = wv > 0 ? edge_prev[((wu * nwv + wv - 1) * 2 + 1) * RW + k] : INF;
+                const float eR =
+                    wv + 1 < nwv ? edge_prev[((wu * nwv + wv + 1) * 2 + 0) * RW + k] : INF;
+                make_window(P[k], eL, eR, lane, pw);
+                if (kI) {
+                    const float iL = sip[(r0 + k + 1) * kIW + 3];
+                    const float iR = sip[(r0 + k + 1) * kIW + 4 + kWV];
+                    make_window(IP[k], iL, iR, lane, iw);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 6; ++i) iw[i] = 0.0f;
+                }
+                // prev row k feeds output rows k-1 (du=+1), k (du=0), k+1 (du=-1)
+                if (k - 1 >= 0) relax_row<KIND, F64>(acc[k - 1], pw, iw, ic[k - 1], +1, p);
+                relax_row<KIND, F64>(acc[k], pw, iw, ic[k], 0, p);
+                if (k + 1 < RW) relax_row<KIND, F64>(acc[k + 1], pw, iw, ic[k + 1], -1, p);
+            }
+            // rows of the neighbouring warp rows (previous step, shared memory)
+            if (!top_warp) {
+                const float* rp = rows_prev + ((wu - 1) * 2 + 1) * VW;  // last row of warp row wu-1
+                const float4 q4 = *reinterpret_cast<const float4*>(rp + vl);
+                const float c4[kC] = {q4.x, q4.y, q4.z, q4.w};
+                float pw[6], iw[6];
+                make_window(c4, has_left ? rp[vl - 1] : INF, has_right ? rp[vl + kC] : INF, lane,
+                            pw);
+                i_window(r0 - 1, iw);
+                relax_row<KIND, F64>(acc[0], pw, iw, ic[0], -1, p);
+            }
+            if (!bot_warp) {
+                const float* rp = rows_prev + ((wu + 1) * 2 + 0) * VW;  // first row of warp row wu+1
+                const float4 q4 = *reinterpret_cast<const float4*>(rp + vl);
+                const float c4[kC] = {q4.x, q4.y, q4.z, q4.w};
+                float pw[6], iw[6];
+                make_window(c4, has_left ? rp[vl - 1] : INF, has_right ? rp[vl + kC] : INF, lane,
+                            pw);
+                i_window(r0 + RW, iw);
+                relax_row<KIND, F64>(acc[RW - 1], pw, iw, ic[RW - 1], +1, p);
+            }
+
+            // ---- phase B: rows above / below the strip (tagged halo) ---------
+            if (top_warp || bot_warp) {
+                long long spins = 0;
+                // Words a lane does not need hold tag `want` by construction, so the
+                // check is branch-free; a stale window is reloaded whole.
+                auto fresh = [&](const unsigned long long (&h)[6]) {
+                    bool ok = true;
+#pragma unroll
+                    for (int i = 0; i < 6; ++i) {
+                        const bool need = (i > 0 && i < 5) || (i == 0 ? has_left : has_right);
+                        ok = ok && (!need || tag_of(h[i]) == want);
+                    }
+                    return ok;
+                };
+                while (true) {
+                    const bool ok_u = !has_up || fresh(hu);
+                    const bool ok_d = !has_dn || fresh(hd);
+                    if (__all_sync(kFull, ok_u && ok_d)) break;
+                    if (!ok_u) load_halo_row(up_base + hoff, has_left, has_right, hu);
+                    if (!ok_d) load_halo_row(dn_base + hoff, has_left, has_right, hd);
+                    if (++spins > kSpinLimit) __trap();
+                }
+                if (top_warp) {
+                    float pw[6], iw[6];
+#pragma unroll
+                    for (int i = 0; i < 6; ++i) {
+                        const bool need = (i > 0 && i < 5) || (i == 0 ? has_left : has_right);
+                        pw[i] = (has_up && need) ? val_of(hu[i]) : INF;
+                    }
+                    i_window(-1, iw);
                     relax_row<KIND, F64>(acc[0], pw, iw, ic[0], -1, p);
-                else
-                    relax_row<KIND, F64>(acc[R - 1], pw, iw, ic[R - 1], +1, p);
+                }
+                if (bot_warp) {
+                    float pw[6], iw[6];
+#pragma unroll
+                    for (int i = 0; i < 6; ++i) {
+                        const bool need = (i > 0 && i < 5) || (i == 0 ? has_left : has_right);
+                        pw[i] = (has_dn && need) ? val_of(hd[i]) : INF;
+                    }
+                    i_window(R, iw);
+                    relax_row<KIND, F64>(acc[RW - 1], pw, iw, ic[RW - 1], +1, p);
+                }
             }
 #pragma unroll
-            for (int r = 0; r < R; ++r)
+            for (int r = 0; r < RW; ++r)
 #pragma unroll
                 for (int c = 0; c < kC; ++c)
                     N[r][c] = (rowv[r] && colv[c]) ? acc[r][c].final(p) : INF;
         }
 
-        // ---- publish the strip's first / last row: the neighbours' critical path
+        // ---- publish: strip border rows (neighbours' critical path), then smem
         if (j < J) {
             const uint32_t tag = p.tag_base + static_cast<uint32_t>(j);
             unsigned long long* q = self_base + (j & 1) * 2ll * VW;
-            if (has_up) {
+            if (pub_top) {
                 st_tagged2(q, N[0][0], N[0][1], tag);
                 st_tagged2(q + 2, N[0][2], N[0][3], tag);
             }
-            if (has_dn) {
-                st_tagged2(q + VW, N[R - 1][0], N[R - 1][1], tag);
-                st_tagged2(q + VW + 2, N[R - 1][2], N[R - 1][3], tag);
+            if (pub_bot) {
+                st_tagged2(q + VW, N[RW - 1][0], N[RW - 1][1], tag);
+                st_tagged2(q + VW + 2, N[RW - 1][2], N[RW - 1][3], tag);
             }
-            float* e = edge + (j & 1) * nwv * 2 * R;
+            float* rw_ = rows + (j & 1) * NWU * 2 * VW + wu * 2 * VW;
+            if (NWU > 1) {
+                *reinterpret_cast<float4*>(rw_ + vl) =
+                    make_float4(N[0][0], N[0][1], N[0][2], N[0][3]);
+                *reinterpret_cast<float4*>(rw_ + VW + vl) =
+                    make_float4(N[RW - 1][0], N[RW - 1][1], N[RW - 1][2], N[RW - 1][3]);
+            }
+            float* e = edge + (j & 1) * NWU * nwv * 2 * RW + (wu * nwv + wv) * 2 * RW;
             if (lane == 0) {
 #pragma unroll
-                for (int r = 0; r < R; ++r) e[(w * 2 + 0) * R + r] = N[r][0];
+                for (int r = 0; r < RW; ++r) e[r] = N[r][0];
             }
             if (lane == 31) {
 #pragma unroll
-                for (int r = 0; r < R; ++r) e[(w * 2 + 1) * R + r] = N[r][kC - 1];
+                for (int r = 0; r < RW; ++r) e[RW + r] = N[r][kC - 1];
             }
         }
 
@@ -404,9 +456,9 @@ __global__ void __launch_bounds__(MW * 32, 1)
             float* base = p.dist + static_cast<long long>(b) * p.vol_stride +
                           static_cast<long long>(s) * p.ss + vl;
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
+            for (int r = 0; r < RW; ++r) {
                 if (!rowv[r]) continue;
-                float* q = base + static_cast<long long>(u0 + r) * p.su;
+                float* q = base + static_cast<long long>(u0 + r0 + r) * p.su;
                 if (colv[kC - 1]) {
                     *reinterpret_cast<float4*>(q) = make_float4(N[r][0], N[r][1], N[r][2], N[r][3]);
                 } else {
@@ -419,7 +471,7 @@ __global__ void __launch_bounds__(MW * 32, 1)
         }
 
 #pragma unroll
-        for (int r = 0; r < R; ++r)
+        for (int r = 0; r < RW; ++r)
 #pragma unroll
             for (int c = 0; c < kC; ++c) {
                 P[r][c] = N[r][c];
@@ -428,11 +480,11 @@ __global__ void __launch_bounds__(MW * 32, 1)
     }
 }
 
-template <int KIND, bool F64, int R, int NST, int MW>
+template <int KIND, bool F64, int RW, int NWU, int NST, int MW>
 cudaError_t launch_one(const CUtensorMap& tm_d, const CUtensorMap& tm_i, const SweepParams& p,
                        cudaStream_t stream) {
-    using L = Layout<R, NST>;
-    auto fn = sweep_kernel<KIND, F64, R, NST, MW>;
+    using L = Layout<RW, NWU, NST>;
+    auto fn = sweep_kernel<KIND, F64, RW, NWU, NST, MW>;
     const size_t smem = L::smem_bytes(p.nwv);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
@@ -440,18 +492,20 @@ cudaError_t launch_one(const CUtensorMap& tm_d, const CUtensorMap& tm_i, const S
     const int grid = p.nvol * p.ntu;
     void* args[] = {const_cast<CUtensorMap*>(&tm_d), const_cast<CUtensorMap*>(&tm_i),
                     const_cast<SweepParams*>(&p)};
-    return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(fn), dim3(grid), dim3(p.nwv * 32),
+    return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(fn), dim3(grid),
+                                       dim3(p.nwv * NWU * 32),
                                        args, smem, stream);
 }
 
-template <int KIND, bool F64, int R, int NST, int MW>
+template <int KIND, bool F64, int RW, int NWU, int NST, int MW>
 int coresident(int nwv) {
-    using L = Layout<R, NST>;
-    auto fn = sweep_kernel<KIND, F64, R, NST, MW>;
+    using L = Layout<RW, NWU, NST>;
+    auto fn = sweep_kernel<KIND, F64, RW, NWU, NST, MW>;
     const size_t smem = L::smem_bytes(nwv);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nwv * 32, smem) != cudaSuccess)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nwv * NWU * 32, smem) !=
+        cudaSuccess)
         return 0;
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
@@ -461,18 +515,23 @@ int coresident(int nwv) {
 
 constexpr int kNST = 4;
 
-// (rows per strip, max warps per strip): narrow planes (<= 512 columns) get the
-// full 255-register budget; wide ones (<= 2048) trade registers for warps.
-#define GD_SWEEP_CASES(X) X(1, 4) X(2, 4) X(4, 4) X(8, 4) X(1, 16) X(2, 16) X(4, 16)
+// Strip shapes (rows per warp RW, warp rows NWU, max warp columns MW): narrow
+// planes (<= 512 columns) run 2 warp rows of 2 rows (R = 4, 2 warps per
+// scheduler); R = 1 serves single-row planes (2D).  Wide planes (<= 2048
+// columns) trade registers for warps.
+#define GD_SWEEP_CASES(X) \
+    X(1, 1, 4) X(2, 1, 4) X(2, 2, 4) X(4, 2, 4) X(1, 1, 16) X(2, 1, 16) X(4, 1, 16)
 
 int width_class(int nwv) { return nwv <= 4 ? 4 : 16; }
 
+// R -> (RW, NWU): 1 -> (1,1), 2 -> (2,1), 4 -> (2,2), 8 -> (4,2)
 template <int KIND, bool F64>
 cudaError_t dispatch_r(int R, const CUtensorMap& tm_d, const CUtensorMap& tm_i,
                        const SweepParams& p, cudaStream_t s) {
     const int mw = width_class(p.nwv);
-#define GD_CASE(RR, MM) \
-    if (R == RR && mw == MM) return launch_one<KIND, F64, RR, kNST, MM>(tm_d, tm_i, p, s);
+#define GD_CASE(RWW, NW, MM)                                         \
+    if (R == RWW * NW && mw == MM)                                   \
+        return launch_one<KIND, F64, RWW, NW, kNST, MM>(tm_d, tm_i, p, s);
     GD_SWEEP_CASES(GD_CASE)
 #undef GD_CASE
     return cudaErrorInvalidValue;
@@ -481,8 +540,8 @@ cudaError_t dispatch_r(int R, const CUtensorMap& tm_d, const CUtensorMap& tm_i,
 template <int KIND, bool F64>
 int dispatch_cores(int R, int nwv) {
     const int mw = width_class(nwv);
-#define GD_CASE(RR, MM) \
-    if (R == RR && mw == MM) return coresident<KIND, F64, RR, kNST, MM>(nwv);
+#define GD_CASE(RWW, NW, MM) \
+    if (R == RWW * NW && mw == MM) return coresident<KIND, F64, RWW, NW, kNST, MM>(nwv);
     GD_SWEEP_CASES(GD_CASE)
 #undef GD_CASE
     return 0;
@@ -506,10 +565,10 @@ cudaError_t launch_sweep(int kind, bool f64, int R, const CUtensorMap& tm_d,
 
 size_t sweep_smem_bytes(int R, int nwv) {
     switch (R) {
-        case 1: return Layout<1, kNST>::smem_bytes(nwv);
-        case 2: return Layout<2, kNST>::smem_bytes(nwv);
-        case 4: return Layout<4, kNST>::smem_bytes(nwv);
-        case 8: return Layout<8, kNST>::smem_bytes(nwv);
+        case 1: return Layout<1, 1, kNST>::smem_bytes(nwv);
+        case 2: return Layout<2, 1, kNST>::smem_bytes(nwv);
+        case 4: return Layout<2, 2, kNST>::smem_bytes(nwv);
+        case 8: return Layout<4, 2, kNST>::smem_bytes(nwv);
     }
     return 0;
 }
