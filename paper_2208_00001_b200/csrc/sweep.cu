@@ -145,7 +145,7 @@ struct Layout {
         return static_cast<size_t>(NST) * nwv * (DBOX + IBOX) * 4     // TMA ring
                + static_cast<size_t>(2) * NWU * 2 * nwv * kWV * 4     // warp-row boundary rows
                + static_cast<size_t>(2) * NWU * nwv * 2 * RW * 4      // warp-edge columns
-               + NST * 8 + 128;
+               + 2 * NST * 8 + 16 + 128;                              // barriers, progress
     }
 };
 
@@ -171,39 +171,54 @@ __device__ __forceinline__ void make_window(const float (&c4)[kC], float edge_l,
     win[5] = lane == 31 ? edge_r : dn;
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void consumer_sync(int nthreads) {
+    asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void st_release_cta(int* p, int v) {
+    asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_cta(const int* p) {
+    int v;
+    asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+    return v;
+}
+
+// Warp-specialised persistent sweep: warps [0, NWU*nwv) relax the strip, the
+// last warp is the TMA producer.  Slot j % NST carries plane p(j); it is
+// released ("empty") by every consumer warp after step j+1, which reads it as
+// the previous plane's intensities.
 template <int KIND, bool F64, int RW, int NWU, int NST, int MW>
-__global__ void __launch_bounds__(MW * NWU * 32, 1)
+__global__ void __launch_bounds__((MW * NWU + 1) * 32, 1)
     sweep_kernel(const __grid_constant__ CUtensorMap tm_d, const __grid_constant__ CUtensorMap tm_i,
                  const __grid_constant__ SweepParams p) {
     using L = Layout<RW, NWU, NST>;
     constexpr int R = L::R, DBOX = L::DBOX, IBOX = L::IBOX;
-    // Spatial (lambda == 0) never reads intensities: only the distance box moves.
-    constexpr uint32_t TXW =
-        static_cast<uint32_t>(KIND == kSpatial ? DBOX * 4 : DBOX * 4 + L::IBYTES);
-    constexpr bool kI = KIND != kSpatial;
+    constexpr bool kI = KIND != kSpatial;  // Spatial never reads intensities
+    constexpr uint32_t TXW = static_cast<uint32_t>(kI ? DBOX * 4 + L::IBYTES : DBOX * 4);
 
     const int nwv = p.nwv;
+    const int ncw = NWU * nwv;  // consumer warps
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const int wu = w / nwv, wv = w - wu * nwv;   // warp row / warp column
-    const int r0 = wu * RW;                      // first strip row of this warp
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float* sd = reinterpret_cast<float*>(smem_raw);     // [NST][nwv][R][128]
     float* si = sd + NST * nwv * DBOX;                   // [NST][nwv][R+2][136]
     float* rows = si + NST * nwv * IBOX;                 // [2][NWU][first|last][nwv*128]
     float* edge = rows + 2 * NWU * 2 * nwv * kWV;        // [2][NWU][nwv][left|right][RW]
-    uint64_t* bar = reinterpret_cast<uint64_t*>(edge + 2 * NWU * nwv * 2 * RW);
+    uint64_t* full = reinterpret_cast<uint64_t*>(edge + 2 * NWU * nwv * 2 * RW);
+    uint64_t* empty = full + NST;
+    int* progress = reinterpret_cast<int*>(empty + NST);
 
     const int g = blockIdx.x;
     const int b = g / p.ntu;
     const int tu = g - b * p.ntu;
     const int u0 = tu * R;
-    const int v0w = wv * kWV;              // first column of this warp
-    const int vl = v0w + kC * lane;         // first column of this lane
     const int n1 = p.ns - 1;
     const int J = p.npass * n1;
-    const float INF = finf();
-    const int VW = nwv * kWV;              // strip width in words / floats
+    const int VW = nwv * kWV;
 
     auto plane_of = [&](int j) -> int {
         if (j <= n1) return p.first_orient > 0 ? j : n1 - j;
@@ -212,42 +227,56 @@ __global__ void __launch_bounds__(MW * NWU * 32, 1)
     };
 
     if (tid == 0) {
-        for (int s = 0; s < NST; ++s) mbar_init(&bar[s], nwv);
+        for (int s = 0; s < NST; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], ncw);
+        }
+        *progress = -1;
         fence_mbar_init();
-    }
-    const bool producer = wu == 0 && lane == 0;  // streams column block wv
-    if (producer) {
-        tma_prefetch_desc(&tm_d);
-        if (kI) tma_prefetch_desc(&tm_i);
     }
     __syncthreads();
 
-    int issued = 0;
-    auto issue = [&](int t) {
-        // Slot j % NST is free once step j-NST+1 (which reads it as the
-        // previous plane) has finished: j <= t + NST - 2 at the top of step t.
-        // A backward-pass plane must first be written by the forward pass
-        // (step 2*n1 - j), i.e. that step must be complete: 2*n1 - j <= t - 1.
-        while (issued <= J && issued <= t + NST - 2) {
-            const int j = issued;
-            if (j > n1 && 2 * n1 - j > t - 1) break;
-            const int slot = j % NST;
-            const int s = plane_of(j);
-            mbar_arrive_expect_tx(&bar[slot], TXW);
-            float* dd = sd + (slot * nwv + wv) * DBOX;
-            float* di = si + (slot * nwv + wv) * IBOX;
-            if (p.tma_sweep_dim == 2) {
-                tma_load_4d(dd, &tm_d, &bar[slot], v0w, u0, s, b);
-                if (kI) tma_load_4d(di, &tm_i, &bar[slot], v0w - 4, u0 - 1, s, b);
-            } else {
-                tma_load_4d(dd, &tm_d, &bar[slot], v0w, s, u0, b);
-                if (kI) tma_load_4d(di, &tm_i, &bar[slot], v0w - 4, s, u0 - 1, b);
+    // ======================= producer warp ==================================
+    if (w == ncw) {
+        if (lane == 0) {
+            tma_prefetch_desc(&tm_d);
+            if (kI) tma_prefetch_desc(&tm_i);
+            for (int j = 0; j <= J; ++j) {
+                const int slot = j % NST, k = j / NST;
+                if (k > 0) mbar_wait(&empty[slot], static_cast<uint32_t>((k - 1) & 1));
+                // A backward-pass plane is the forward pass's output of step 2*n1 - j.
+                if (j > n1) {
+                    const int jf = 2 * n1 - j;
+                    while (ld_acquire_cta(progress) < jf) {
+                    }
+                }
+                const int s = plane_of(j);
+                mbar_arrive_expect_tx(&full[slot], TXW * nwv);
+                for (int cb = 0; cb < nwv; ++cb) {
+                    float* dd = sd + (slot * nwv + cb) * DBOX;
+                    float* di = si + (slot * nwv + cb) * IBOX;
+                    const int v0 = cb * kWV;
+                    if (p.tma_sweep_dim == 2) {
+                        tma_load_4d(dd, &tm_d, &full[slot], v0, u0, s, b);
+                        if (kI) tma_load_4d(di, &tm_i, &full[slot], v0 - 4, u0 - 1, s, b);
+                    } else {
+                        tma_load_4d(dd, &tm_d, &full[slot], v0, s, u0, b);
+                        if (kI) tma_load_4d(di, &tm_i, &full[slot], v0 - 4, s, u0 - 1, b);
+                    }
+                }
             }
-            ++issued;
         }
-    };
+        return;
+    }
 
-    // Tagged halo rows: the strip above publishes its BOT row, the one below its TOP row.
+    // ======================= consumer warps =================================
+    const int wu = w / nwv, wv = w - wu * nwv;   // warp row / warp column
+    const int r0 = wu * RW;                      // first strip row of this warp
+    const int v0w = wv * kWV;
+    const int vl = v0w + kC * lane;
+    const float INF = finf();
+    const int nthreads = ncw * 32;
+
     const bool top_warp = wu == 0, bot_warp = wu == NWU - 1;
     const bool has_up = tu > 0 && top_warp, has_dn = tu + 1 < p.ntu && bot_warp;
     const long long strip_words = 2ll * 2 * VW;  // per strip: 2 parities x {TOP, BOT}
@@ -256,33 +285,103 @@ __global__ void __launch_bounds__(MW * NWU * 32, 1)
     const unsigned long long* dn_base = p.halo + (strip0 + tu + 1) * strip_words + vl;
     unsigned long long* self_base = p.halo + static_cast<long long>(g) * strip_words + vl;
     const bool pub_top = tu > 0 && top_warp, pub_bot = tu + 1 < p.ntu && bot_warp;
-    const bool has_left = vl > 0, has_right = vl + kC < p.nv;  // lane-level edge words
+    const bool has_left = vl > 0, has_right = vl + kC < p.nv;
 
     bool rowv[RW], colv[kC];
 #pragma unroll
     for (int r = 0; r < RW; ++r) rowv[r] = (u0 + r0 + r) < p.nu;
 #pragma unroll
     for (int c = 0; c < kC; ++c) colv[c] = (vl + c) < p.nv;
+    const bool all_valid = __all_sync(kFull, (u0 + r0 + RW <= p.nu) && (vl + kC <= p.nv));
+
+    // global output pointers of this lane's rows, advanced per plane
+    float* outp[RW];
+#pragma unroll
+    for (int r = 0; r < RW; ++r)
+        outp[r] = p.dist + static_cast<long long>(b) * p.vol_stride +
+                  static_cast<long long>(u0 + r0 + r) * p.su + vl;
 
     float P[RW][kC], IP[RW][kC];  // previous plane: new distances / intensities of own voxels
 
-    for (int j = 0; j <= J; ++j) {
-        __syncthreads();  // step j-1 complete: boundary rows/edges visible, slot (j-2)%NST free
-        if (producer) issue(j);
+    // Publishes the strip border rows (tagged, global) and the warp's boundary
+    // rows / edge columns (shared) of plane j.
+    auto publish = [&](int j, const float (&N)[RW][kC]) {
+        if (j < J) {
+            const uint32_t tag = p.tag_base + static_cast<uint32_t>(j);
+            unsigned long long* q = self_base + (j & 1) * 2ll * VW;
+            if (pub_top) {
+                st_tagged2(q, N[0][0], N[0][1], tag);
+                st_tagged2(q + 2, N[0][2], N[0][3], tag);
+            }
+            if (pub_bot) {
+                st_tagged2(q + VW, N[RW - 1][0], N[RW - 1][1], tag);
+                st_tagged2(q + VW + 2, N[RW - 1][2], N[RW - 1][3], tag);
+            }
+            if (NWU > 1) {
+                float* rw_ = rows + (j & 1) * NWU * 2 * VW + wu * 2 * VW;
+                *reinterpret_cast<float4*>(rw_ + vl) =
+                    make_float4(N[0][0], N[0][1], N[0][2], N[0][3]);
+                *reinterpret_cast<float4*>(rw_ + VW + vl) =
+                    make_float4(N[RW - 1][0], N[RW - 1][1], N[RW - 1][2], N[RW - 1][3]);
+            }
+            float* e = edge + (j & 1) * NWU * nwv * 2 * RW + (wu * nwv + wv) * 2 * RW;
+#pragma unroll
+            for (int r = 0; r < RW; ++r) {
+                if (lane == 0) e[r] = N[r][0];
+                if (lane == 31) e[RW + r] = N[r][kC - 1];
+            }
+        }
+    };
 
+    // ---- step 0: the first plane is final as loaded --------------------------
+    {
+        mbar_wait(&full[0], 0u);
+        const float* sdc = sd + wv * DBOX;
+        const float* sic = si + wv * IBOX;
+        float N[RW][kC];
+#pragma unroll
+        for (int r = 0; r < RW; ++r) {
+            const float4 d4 = *reinterpret_cast<const float4*>(sdc + (r0 + r) * kWV + kC * lane);
+            N[r][0] = d4.x; N[r][1] = d4.y; N[r][2] = d4.z; N[r][3] = d4.w;
+            if (kI) {
+                const float4 i4 = *reinterpret_cast<const float4*>(sic + (r0 + r + 1) * kIW + 4 +
+                                                                   kC * lane);
+                IP[r][0] = i4.x; IP[r][1] = i4.y; IP[r][2] = i4.z; IP[r][3] = i4.w;
+            } else {
+#pragma unroll
+                for (int c = 0; c < kC; ++c) IP[r][c] = 0.0f;
+            }
+#pragma unroll
+            for (int c = 0; c < kC; ++c)
+                if (!(rowv[r] && colv[c])) N[r][c] = INF;
+        }
+        publish(0, N);
+#pragma unroll
+        for (int r = 0; r < RW; ++r)
+#pragma unroll
+            for (int c = 0; c < kC; ++c) P[r][c] = N[r][c];
+        consumer_sync(nthreads);
+    }
+
+    int slot = 0;
+    uint32_t phase = 0;
+    for (int j = 1; j <= J; ++j) {
+        const int pslot = slot;  // previous plane's slot
+        if (++slot == NST) {
+            slot = 0;
+            phase ^= 1u;
+        }
         const int par = (j - 1) & 1;
         const long long hoff = par * 2ll * VW;
         const uint32_t want = p.tag_base + static_cast<uint32_t>(j - 1);
         unsigned long long hu[6], hd[6];  // [0] = v-1, [1..4] own, [5] = v+4
-        if (j > 0) {
-            if (has_up) load_halo_row(up_base + hoff, has_left, has_right, hu);
-            if (has_dn) load_halo_row(dn_base + hoff, has_left, has_right, hd);
-        }
+        if (has_up) load_halo_row(up_base + hoff, has_left, has_right, hu);
+        if (has_dn) load_halo_row(dn_base + hoff, has_left, has_right, hd);
 
-        const int slot = j % NST;
-        mbar_wait(&bar[slot], static_cast<uint32_t>((j / NST) & 1));
+        mbar_wait(&full[slot], phase);
         const float* sdc = sd + (slot * nwv + wv) * DBOX;
         const float* sic = si + (slot * nwv + wv) * IBOX;
+        const float* sip = si + (pslot * nwv + wv) * IBOX;  // previous plane's I box
         float dold[RW][kC], ic[RW][kC];
 #pragma unroll
         for (int r = 0; r < RW; ++r) {
@@ -298,121 +397,114 @@ __global__ void __launch_bounds__(MW * NWU * 32, 1)
             }
         }
 
-        float N[RW][kC];
-        if (j == 0) {
+        const float* rows_prev = rows + par * NWU * 2 * VW;
+        const float* edge_prev = edge + par * NWU * nwv * 2 * RW;
+        Acc<KIND, F64> acc[RW][kC];
 #pragma unroll
-            for (int r = 0; r < RW; ++r)
+        for (int r = 0; r < RW; ++r)
 #pragma unroll
-                for (int c = 0; c < kC; ++c) N[r][c] = (rowv[r] && colv[c]) ? dold[r][c] : INF;
-        } else {
-            const float* sip = si + (((j - 1) % NST) * nwv + wv) * IBOX;  // previous plane's I box
-            const float* rows_prev = rows + par * NWU * 2 * VW;
-            const float* edge_prev = edge + par * NWU * nwv * 2 * RW;
-            Acc<KIND, F64> acc[RW][kC];
-#pragma unroll
-            for (int r = 0; r < RW; ++r)
-#pragma unroll
-                for (int c = 0; c < kC; ++c) acc[r][c].init(dold[r][c]);
+            for (int c = 0; c < kC; ++c) acc[r][c].init(dold[r][c]);
 
-            // Intensity window of previous-plane strip row `sr` (box row sr+1).
-            auto i_window = [&](int sr, float (&iw)[6]) {
-                if (kI) {
-                    const float* rp = sip + (sr + 1) * kIW;
-                    const float4 i4 = *reinterpret_cast<const float4*>(rp + 4 + kC * lane);
-                    const float c4[kC] = {i4.x, i4.y, i4.z, i4.w};
-                    make_window(c4, rp[3], rp[4 + kWV], lane, iw);
-                } else {
+        // Intensity window of previous-plane strip row `sr` (box row sr+1).
+        auto i_window = [&](int sr, float (&iw)[6]) {
+            if (kI) {
+                const float* rp = sip + (sr + 1) * kIW;
+                const float4 i4 = *reinterpret_cast<const float4*>(rp + 4 + kC * lane);
+                const float c4[kC] = {i4.x, i4.y, i4.z, i4.w};
+                make_window(c4, rp[3], rp[4 + kWV], lane, iw);
+            } else {
 #pragma unroll
-                    for (int i = 0; i < 6; ++i) iw[i] = 0.0f;
-                }
-            };
-
-            // ---- phase A: previous-plane rows held inside the CTA ------------
-#pragma unroll
-            for (int k = 0; k < RW; ++k) {
-                float pw[6], iw[6];
-                const float eL = wv > 0 ? edge_prev[((wu * nwv + wv - 1) * 2 + 1) * RW + k] : INF;
-                const float eR =
-                    wv + 1 < nwv ? edge_prev[((wu * nwv + wv + 1) * 2 + 0) * RW + k] : INF;
-                make_window(P[k], eL, eR, lane, pw);
-                if (kI) {
-                    const float iL = sip[(r0 + k + 1) * kIW + 3];
-                    const float iR = sip[(r0 + k + 1) * kIW + 4 + kWV];
-                    make_window(IP[k], iL, iR, lane, iw);
-                } else {
-#pragma unroll
-                    for (int i = 0; i < 6; ++i) iw[i] = 0.0f;
-                }
-                // prev row k feeds output rows k-1 (du=+1), k (du=0), k+1 (du=-1)
-                if (k - 1 >= 0) relax_row<KIND, F64>(acc[k - 1], pw, iw, ic[k - 1], +1, p);
-                relax_row<KIND, F64>(acc[k], pw, iw, ic[k], 0, p);
-                if (k + 1 < RW) relax_row<KIND, F64>(acc[k + 1], pw, iw, ic[k + 1], -1, p);
+                for (int i = 0; i < 6; ++i) iw[i] = 0.0f;
             }
-            // rows of the neighbouring warp rows (previous step, shared memory)
-            if (!top_warp) {
-                const float* rp = rows_prev + ((wu - 1) * 2 + 1) * VW;  // last row of warp row wu-1
-                const float4 q4 = *reinterpret_cast<const float4*>(rp + vl);
-                const float c4[kC] = {q4.x, q4.y, q4.z, q4.w};
+        };
+
+        // ---- phase A: previous-plane rows held inside the CTA ----------------
+#pragma unroll
+        for (int k = 0; k < RW; ++k) {
+            float pw[6], iw[6];
+            const float eL = wv > 0 ? edge_prev[((wu * nwv + wv - 1) * 2 + 1) * RW + k] : INF;
+            const float eR = wv + 1 < nwv ? edge_prev[((wu * nwv + wv + 1) * 2 + 0) * RW + k] : INF;
+            make_window(P[k], eL, eR, lane, pw);
+            if (kI) {
+                const float* rp = sip + (r0 + k + 1) * kIW;
+                make_window(IP[k], rp[3], rp[4 + kWV], lane, iw);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 6; ++i) iw[i] = 0.0f;
+            }
+            // prev row k feeds output rows k-1 (du=+1), k (du=0), k+1 (du=-1)
+            if (k - 1 >= 0) relax_row<KIND, F64>(acc[k - 1], pw, iw, ic[k - 1], +1, p);
+            relax_row<KIND, F64>(acc[k], pw, iw, ic[k], 0, p);
+            if (k + 1 < RW) relax_row<KIND, F64>(acc[k + 1], pw, iw, ic[k + 1], -1, p);
+        }
+        if (!top_warp) {
+            const float* rp = rows_prev + ((wu - 1) * 2 + 1) * VW;  // last row of warp row wu-1
+            const float4 q4 = *reinterpret_cast<const float4*>(rp + vl);
+            const float c4[kC] = {q4.x, q4.y, q4.z, q4.w};
+            float pw[6], iw[6];
+            make_window(c4, has_left ? rp[vl - 1] : INF, has_right ? rp[vl + kC] : INF, lane, pw);
+            i_window(r0 - 1, iw);
+            relax_row<KIND, F64>(acc[0], pw, iw, ic[0], -1, p);
+        }
+        if (!bot_warp) {
+            const float* rp = rows_prev + ((wu + 1) * 2 + 0) * VW;  // first row of warp row wu+1
+            const float4 q4 = *reinterpret_cast<const float4*>(rp + vl);
+            const float c4[kC] = {q4.x, q4.y, q4.z, q4.w};
+            float pw[6], iw[6];
+            make_window(c4, has_left ? rp[vl - 1] : INF, has_right ? rp[vl + kC] : INF, lane, pw);
+            i_window(r0 + RW, iw);
+            relax_row<KIND, F64>(acc[RW - 1], pw, iw, ic[RW - 1], +1, p);
+        }
+
+        // ---- phase B: rows above / below the strip (tagged halo) -------------
+        if (top_warp || bot_warp) {
+            auto fresh = [&](const unsigned long long (&h)[6]) {
+                bool ok = true;
+#pragma unroll
+                for (int i = 0; i < 6; ++i) {
+                    const bool need = (i > 0 && i < 5) || (i == 0 ? has_left : has_right);
+                    ok = ok && (!need || tag_of(h[i]) == want);
+                }
+                return ok;
+            };
+            long long spins = 0;
+            while (true) {
+                const bool ok_u = !has_up || fresh(hu);
+                const bool ok_d = !has_dn || fresh(hd);
+                if (__all_sync(kFull, ok_u && ok_d)) break;
+                if (!ok_u) load_halo_row(up_base + hoff, has_left, has_right, hu);
+                if (!ok_d) load_halo_row(dn_base + hoff, has_left, has_right, hd);
+                if (++spins > kSpinLimit) __trap();
+            }
+            if (top_warp) {
                 float pw[6], iw[6];
-                make_window(c4, has_left ? rp[vl - 1] : INF, has_right ? rp[vl + kC] : INF, lane,
-                            pw);
-                i_window(r0 - 1, iw);
+#pragma unroll
+                for (int i = 0; i < 6; ++i) {
+                    const bool need = (i > 0 && i < 5) || (i == 0 ? has_left : has_right);
+                    pw[i] = (has_up && need) ? val_of(hu[i]) : INF;
+                }
+                i_window(-1, iw);
                 relax_row<KIND, F64>(acc[0], pw, iw, ic[0], -1, p);
             }
-            if (!bot_warp) {
-                const float* rp = rows_prev + ((wu + 1) * 2 + 0) * VW;  // first row of warp row wu+1
-                const float4 q4 = *reinterpret_cast<const float4*>(rp + vl);
-                const float c4[kC] = {q4.x, q4.y, q4.z, q4.w};
+            if (bot_warp) {
                 float pw[6], iw[6];
-                make_window(c4, has_left ? rp[vl - 1] : INF, has_right ? rp[vl + kC] : INF, lane,
-                            pw);
-                i_window(r0 + RW, iw);
+#pragma unroll
+                for (int i = 0; i < 6; ++i) {
+                    const bool need = (i > 0 && i < 5) || (i == 0 ? has_left : has_right);
+                    pw[i] = (has_dn && need) ? val_of(hd[i]) : INF;
+                }
+                i_window(R, iw);
                 relax_row<KIND, F64>(acc[RW - 1], pw, iw, ic[RW - 1], +1, p);
             }
+        }
 
-            // ---- phase B: rows above / below the strip (tagged halo) ---------
-            if (top_warp || bot_warp) {
-                long long spins = 0;
-                // Words a lane does not need hold tag `want` by construction, so the
-                // check is branch-free; a stale window is reloaded whole.
-                auto fresh = [&](const unsigned long long (&h)[6]) {
-                    bool ok = true;
+        float N[RW][kC];
+        if (all_valid) {
 #pragma unroll
-                    for (int i = 0; i < 6; ++i) {
-                        const bool need = (i > 0 && i < 5) || (i == 0 ? has_left : has_right);
-                        ok = ok && (!need || tag_of(h[i]) == want);
-                    }
-                    return ok;
-                };
-                while (true) {
-                    const bool ok_u = !has_up || fresh(hu);
-                    const bool ok_d = !has_dn || fresh(hd);
-                    if (__all_sync(kFull, ok_u && ok_d)) break;
-                    if (!ok_u) load_halo_row(up_base + hoff, has_left, has_right, hu);
-                    if (!ok_d) load_halo_row(dn_base + hoff, has_left, has_right, hd);
-                    if (++spins > kSpinLimit) __trap();
-                }
-                if (top_warp) {
-                    float pw[6], iw[6];
+            for (int r = 0; r < RW; ++r)
 #pragma unroll
-                    for (int i = 0; i < 6; ++i) {
-                        const bool need = (i > 0 && i < 5) || (i == 0 ? has_left : has_right);
-                        pw[i] = (has_up && need) ? val_of(hu[i]) : INF;
-                    }
-                    i_window(-1, iw);
-                    relax_row<KIND, F64>(acc[0], pw, iw, ic[0], -1, p);
-                }
-                if (bot_warp) {
-                    float pw[6], iw[6];
-#pragma unroll
-                    for (int i = 0; i < 6; ++i) {
-                        const bool need = (i > 0 && i < 5) || (i == 0 ? has_left : has_right);
-                        pw[i] = (has_dn && need) ? val_of(hd[i]) : INF;
-                    }
-                    i_window(R, iw);
-                    relax_row<KIND, F64>(acc[RW - 1], pw, iw, ic[RW - 1], +1, p);
-                }
-            }
+                for (int c = 0; c < kC; ++c) N[r][c] = acc[r][c].final(p);
+        } else {
 #pragma unroll
             for (int r = 0; r < RW; ++r)
 #pragma unroll
@@ -420,45 +512,20 @@ __global__ void __launch_bounds__(MW * NWU * 32, 1)
                     N[r][c] = (rowv[r] && colv[c]) ? acc[r][c].final(p) : INF;
         }
 
-        // ---- publish: strip border rows (neighbours' critical path), then smem
-        if (j < J) {
-            const uint32_t tag = p.tag_base + static_cast<uint32_t>(j);
-            unsigned long long* q = self_base + (j & 1) * 2ll * VW;
-            if (pub_top) {
-                st_tagged2(q, N[0][0], N[0][1], tag);
-                st_tagged2(q + 2, N[0][2], N[0][3], tag);
-            }
-            if (pub_bot) {
-                st_tagged2(q + VW, N[RW - 1][0], N[RW - 1][1], tag);
-                st_tagged2(q + VW + 2, N[RW - 1][2], N[RW - 1][3], tag);
-            }
-            float* rw_ = rows + (j & 1) * NWU * 2 * VW + wu * 2 * VW;
-            if (NWU > 1) {
-                *reinterpret_cast<float4*>(rw_ + vl) =
-                    make_float4(N[0][0], N[0][1], N[0][2], N[0][3]);
-                *reinterpret_cast<float4*>(rw_ + VW + vl) =
-                    make_float4(N[RW - 1][0], N[RW - 1][1], N[RW - 1][2], N[RW - 1][3]);
-            }
-            float* e = edge + (j & 1) * NWU * nwv * 2 * RW + (wu * nwv + wv) * 2 * RW;
-            if (lane == 0) {
-#pragma unroll
-                for (int r = 0; r < RW; ++r) e[r] = N[r][0];
-            }
-            if (lane == 31) {
-#pragma unroll
-                for (int r = 0; r < RW; ++r) e[RW + r] = N[r][kC - 1];
-            }
-        }
+        publish(j, N);
 
         // ---- store the relaxed plane ------------------------------------------
-        if (j > 0) {
-            const int s = plane_of(j);
-            float* base = p.dist + static_cast<long long>(b) * p.vol_stride +
-                          static_cast<long long>(s) * p.ss + vl;
+        const long long soff = static_cast<long long>(plane_of(j)) * p.ss;
+        if (all_valid) {
+#pragma unroll
+            for (int r = 0; r < RW; ++r)
+                *reinterpret_cast<float4*>(outp[r] + soff) =
+                    make_float4(N[r][0], N[r][1], N[r][2], N[r][3]);
+        } else {
 #pragma unroll
             for (int r = 0; r < RW; ++r) {
                 if (!rowv[r]) continue;
-                float* q = base + static_cast<long long>(u0 + r0 + r) * p.su;
+                float* q = outp[r] + soff;
                 if (colv[kC - 1]) {
                     *reinterpret_cast<float4*>(q) = make_float4(N[r][0], N[r][1], N[r][2], N[r][3]);
                 } else {
@@ -467,8 +534,13 @@ __global__ void __launch_bounds__(MW * NWU * 32, 1)
                         if (colv[c]) q[c] = N[r][c];
                 }
             }
-            if (p.fence_turn && j <= n1) fence_proxy_async_global();
         }
+        if (p.fence_turn && j <= n1) fence_proxy_async_global();
+
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[pslot]);  // previous plane's slot fully consumed
+        consumer_sync(nthreads);
+        if (tid == 0) st_release_cta(progress, j);
 
 #pragma unroll
         for (int r = 0; r < RW; ++r)
@@ -493,7 +565,7 @@ cudaError_t launch_one(const CUtensorMap& tm_d, const CUtensorMap& tm_i, const S
     void* args[] = {const_cast<CUtensorMap*>(&tm_d), const_cast<CUtensorMap*>(&tm_i),
                     const_cast<SweepParams*>(&p)};
     return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(fn), dim3(grid),
-                                       dim3(p.nwv * NWU * 32),
+                                       dim3((p.nwv * NWU + 1) * 32),
                                        args, smem, stream);
 }
 
@@ -504,7 +576,7 @@ int coresident(int nwv) {
     const size_t smem = L::smem_bytes(nwv);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nwv * NWU * 32, smem) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, (nwv * NWU + 1) * 32, smem) !=
         cudaSuccess)
         return 0;
     int dev = 0, sms = 0;
