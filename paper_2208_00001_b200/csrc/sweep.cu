@@ -172,7 +172,9 @@ __device__ __forceinline__ void make_window(const float (&c4)[kC], float edge_l,
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+    // relaxed: only smem reads (already consumed) precede it; a release arrive
+    // would wait (MEMBAR) on this thread's outstanding global stores.
+    asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void consumer_sync(int nthreads) {
     asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
@@ -186,226 +188,196 @@ __device__ __forceinline__ int ld_acquire_cta(const int* p) {
     return v;
 }
 
-// Warp-specialised persistent sweep: warps [0, NWU*nwv) relax the strip, the
-// last warp is the TMA producer.  Slot j % NST carries plane p(j); it is
-// released ("empty") by every consumer warp after step j+1, which reads it as
-// the previous plane's intensities.
-template <int KIND, bool F64, int RW, int NWU, int NST, int MW>
-__global__ void __launch_bounds__((MW * NWU + 1) * 32, 1)
-    sweep_kernel(const __grid_constant__ CUtensorMap tm_d, const __grid_constant__ CUtensorMap tm_i,
-                 const __grid_constant__ SweepParams p) {
+// Shared-memory carve-up and launch geometry, common to producer and consumers.
+template <int RW, int NWU, int NST>
+struct Ctx {
+    float* sd;          // [NST][nwv][R][128]      old distances (TMA)
+    float* si;          // [NST][nwv][R+2][136]    intensities + row halo (TMA)
+    float* rows;        // [2][NWU][first|last][nwv*128] warp-row boundary rows
+    float* edge;        // [2][NWU][nwv][left|right][RW] warp-edge columns
+    uint64_t* full;     // [NST]
+    uint64_t* empty;    // [NST]
+    int* progress;
+    int nwv, g, b, tu, u0, n1, J, VW;
+};
+
+template <int RW, int NWU, int NST>
+__device__ __forceinline__ int plane_of(const SweepParams& p, const Ctx<RW, NWU, NST>& c, int j) {
+    if (j <= c.n1) return p.first_orient > 0 ? j : c.n1 - j;
+    const int k = j - c.n1;
+    return p.first_orient > 0 ? c.n1 - k : k;
+}
+
+// One consumer warp's whole sweep.  TOP / BOT: the warp row borders the strip
+// above / below (tagged global halo); FULL: every voxel of the warp is inside
+// the volume.  Specialising on the role keeps the per-step body branch-free.
+template <int KIND, bool F64, int RW, int NWU, int NST, bool TOP, bool BOT, bool FULL>
+__device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW, NWU, NST>& c,
+                                              int wu, int wv, int lane) {
     using L = Layout<RW, NWU, NST>;
     constexpr int R = L::R, DBOX = L::DBOX, IBOX = L::IBOX;
-    constexpr bool kI = KIND != kSpatial;  // Spatial never reads intensities
-    constexpr uint32_t TXW = static_cast<uint32_t>(kI ? DBOX * 4 + L::IBYTES : DBOX * 4);
-
-    const int nwv = p.nwv;
-    const int ncw = NWU * nwv;  // consumer warps
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    float* sd = reinterpret_cast<float*>(smem_raw);     // [NST][nwv][R][128]
-    float* si = sd + NST * nwv * DBOX;                   // [NST][nwv][R+2][136]
-    float* rows = si + NST * nwv * IBOX;                 // [2][NWU][first|last][nwv*128]
-    float* edge = rows + 2 * NWU * 2 * nwv * kWV;        // [2][NWU][nwv][left|right][RW]
-    uint64_t* full = reinterpret_cast<uint64_t*>(edge + 2 * NWU * nwv * 2 * RW);
-    uint64_t* empty = full + NST;
-    int* progress = reinterpret_cast<int*>(empty + NST);
-
-    const int g = blockIdx.x;
-    const int b = g / p.ntu;
-    const int tu = g - b * p.ntu;
-    const int u0 = tu * R;
-    const int n1 = p.ns - 1;
-    const int J = p.npass * n1;
-    const int VW = nwv * kWV;
-
-    auto plane_of = [&](int j) -> int {
-        if (j <= n1) return p.first_orient > 0 ? j : n1 - j;
-        const int k = j - n1;
-        return p.first_orient > 0 ? n1 - k : k;
-    };
-
-    if (tid == 0) {
-        for (int s = 0; s < NST; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], ncw);
-        }
-        *progress = -1;
-        fence_mbar_init();
-    }
-    __syncthreads();
-
-    // ======================= producer warp ==================================
-    if (w == ncw) {
-        if (lane == 0) {
-            tma_prefetch_desc(&tm_d);
-            if (kI) tma_prefetch_desc(&tm_i);
-            for (int j = 0; j <= J; ++j) {
-                const int slot = j % NST, k = j / NST;
-                if (k > 0) mbar_wait(&empty[slot], static_cast<uint32_t>((k - 1) & 1));
-                // A backward-pass plane is the forward pass's output of step 2*n1 - j.
-                if (j > n1) {
-                    const int jf = 2 * n1 - j;
-                    while (ld_acquire_cta(progress) < jf) {
-                    }
-                }
-                const int s = plane_of(j);
-                mbar_arrive_expect_tx(&full[slot], TXW * nwv);
-                for (int cb = 0; cb < nwv; ++cb) {
-                    float* dd = sd + (slot * nwv + cb) * DBOX;
-                    float* di = si + (slot * nwv + cb) * IBOX;
-                    const int v0 = cb * kWV;
-                    if (p.tma_sweep_dim == 2) {
-                        tma_load_4d(dd, &tm_d, &full[slot], v0, u0, s, b);
-                        if (kI) tma_load_4d(di, &tm_i, &full[slot], v0 - 4, u0 - 1, s, b);
-                    } else {
-                        tma_load_4d(dd, &tm_d, &full[slot], v0, s, u0, b);
-                        if (kI) tma_load_4d(di, &tm_i, &full[slot], v0 - 4, s, u0 - 1, b);
-                    }
-                }
-            }
-        }
-        return;
-    }
-
-    // ======================= consumer warps =================================
-    const int wu = w / nwv, wv = w - wu * nwv;   // warp row / warp column
-    const int r0 = wu * RW;                      // first strip row of this warp
-    const int v0w = wv * kWV;
-    const int vl = v0w + kC * lane;
+    constexpr bool kI = KIND != kSpatial;
+    const int nwv = c.nwv, VW = c.VW, J = c.J, n1 = c.n1;
+    const int r0 = wu * RW;
+    const int vl = wv * kWV + kC * lane;
     const float INF = finf();
-    const int nthreads = ncw * 32;
+    const int nthreads = NWU * nwv * 32;
+    const int tid = (wu * nwv + wv) * 32 + lane;
+    const uint32_t tag_base = p.tag_base;
+    const bool turn_fence = p.fence_turn != 0;
 
-    const bool top_warp = wu == 0, bot_warp = wu == NWU - 1;
-    const bool has_up = tu > 0 && top_warp, has_dn = tu + 1 < p.ntu && bot_warp;
+    const bool has_up = TOP && c.tu > 0, has_dn = BOT && c.tu + 1 < p.ntu;
     const long long strip_words = 2ll * 2 * VW;  // per strip: 2 parities x {TOP, BOT}
-    const long long strip0 = static_cast<long long>(b) * p.ntu;
-    const unsigned long long* up_base = p.halo + (strip0 + tu - 1) * strip_words + VW + vl;
-    const unsigned long long* dn_base = p.halo + (strip0 + tu + 1) * strip_words + vl;
-    unsigned long long* self_base = p.halo + static_cast<long long>(g) * strip_words + vl;
-    const bool pub_top = tu > 0 && top_warp, pub_bot = tu + 1 < p.ntu && bot_warp;
+    const long long strip0 = static_cast<long long>(c.b) * p.ntu;
+    // Halo row windows, one pointer per parity.  Lanes at the plane's edge
+    // point their v-1 / v+4 word at their own first word (value unused).
     const bool has_left = vl > 0, has_right = vl + kC < p.nv;
+    const int dl = has_left ? -1 : 0, dr = has_right ? kC : 0;
+    const unsigned long long* up0 = p.halo + (strip0 + c.tu - 1) * strip_words + VW + vl;
+    const unsigned long long* dn0 = p.halo + (strip0 + c.tu + 1) * strip_words + vl;
+    unsigned long long* self0 = p.halo + static_cast<long long>(c.g) * strip_words + vl;
+    const bool pub_up = TOP && c.tu > 0, pub_dn = BOT && c.tu + 1 < p.ntu;
+    // neighbour-warp edge columns
+    const int eoffL = ((wu * nwv + wv - 1) * 2 + 1) * RW;
+    const int eoffR = ((wu * nwv + wv + 1) * 2 + 0) * RW;
+    const bool wl = wv > 0, wr = wv + 1 < nwv;
+    float* const edge_own = c.edge + (wu * nwv + wv) * 2 * RW;
+    const int EPAR = NWU * nwv * 2 * RW;  // edge buffer parity stride
+    const int RPAR = NWU * 2 * VW;        // rows buffer parity stride
 
     bool rowv[RW], colv[kC];
 #pragma unroll
-    for (int r = 0; r < RW; ++r) rowv[r] = (u0 + r0 + r) < p.nu;
+    for (int r = 0; r < RW; ++r) rowv[r] = (c.u0 + r0 + r) < p.nu;
 #pragma unroll
-    for (int c = 0; c < kC; ++c) colv[c] = (vl + c) < p.nv;
-    const bool all_valid = __all_sync(kFull, (u0 + r0 + RW <= p.nu) && (vl + kC <= p.nv));
+    for (int q = 0; q < kC; ++q) colv[q] = (vl + q) < p.nv;
 
-    // global output pointers of this lane's rows, advanced per plane
-    float* outp[RW];
-#pragma unroll
-    for (int r = 0; r < RW; ++r)
-        outp[r] = p.dist + static_cast<long long>(b) * p.vol_stride +
-                  static_cast<long long>(u0 + r0 + r) * p.su + vl;
+    // Output pointer of this lane's first row at the current plane; rows are su apart.
+    const long long su = p.su;
+    float* outp = p.dist + static_cast<long long>(c.b) * p.vol_stride +
+                  static_cast<long long>(c.u0 + r0) * su + vl +
+                  static_cast<long long>(plane_of(p, c, 0)) * p.ss;
+    long long dsoff = p.first_orient > 0 ? p.ss : -p.ss;
 
-    float P[RW][kC], IP[RW][kC];  // previous plane: new distances / intensities of own voxels
+    // Shared-memory slot pointers (this warp's column block).
+    const float* const sd_base = c.sd + wv * DBOX;
+    const float* const si_base = c.si + wv * IBOX;
+    const int SD_STRIDE = nwv * DBOX, SI_STRIDE = nwv * IBOX;
 
-    // Publishes the strip border rows (tagged, global) and the warp's boundary
-    // rows / edge columns (shared) of plane j.
     auto publish = [&](int j, const float (&N)[RW][kC]) {
-        if (j < J) {
-            const uint32_t tag = p.tag_base + static_cast<uint32_t>(j);
-            unsigned long long* q = self_base + (j & 1) * 2ll * VW;
-            if (pub_top) {
-                st_tagged2(q, N[0][0], N[0][1], tag);
-                st_tagged2(q + 2, N[0][2], N[0][3], tag);
-            }
-            if (pub_bot) {
-                st_tagged2(q + VW, N[RW - 1][0], N[RW - 1][1], tag);
-                st_tagged2(q + VW + 2, N[RW - 1][2], N[RW - 1][3], tag);
-            }
-            if (NWU > 1) {
-                float* rw_ = rows + (j & 1) * NWU * 2 * VW + wu * 2 * VW;
+        const int par = j & 1;
+        const uint32_t tag = tag_base + static_cast<uint32_t>(j);
+        unsigned long long* q = self0 + par * 2ll * VW;
+        if (pub_up) {
+            st_tagged2(q, N[0][0], N[0][1], tag);
+            st_tagged2(q + 2, N[0][2], N[0][3], tag);
+        }
+        if (pub_dn) {
+            st_tagged2(q + VW, N[RW - 1][0], N[RW - 1][1], tag);
+            st_tagged2(q + VW + 2, N[RW - 1][2], N[RW - 1][3], tag);
+        }
+        if (NWU > 1) {
+            float* rw_ = c.rows + par * RPAR + wu * 2 * VW;
+            if (!TOP)
                 *reinterpret_cast<float4*>(rw_ + vl) =
                     make_float4(N[0][0], N[0][1], N[0][2], N[0][3]);
+            if (!BOT)
                 *reinterpret_cast<float4*>(rw_ + VW + vl) =
                     make_float4(N[RW - 1][0], N[RW - 1][1], N[RW - 1][2], N[RW - 1][3]);
-            }
-            float* e = edge + (j & 1) * NWU * nwv * 2 * RW + (wu * nwv + wv) * 2 * RW;
+        }
+        float* e = edge_own + par * EPAR;
 #pragma unroll
-            for (int r = 0; r < RW; ++r) {
-                if (lane == 0) e[r] = N[r][0];
-                if (lane == 31) e[RW + r] = N[r][kC - 1];
-            }
+        for (int r = 0; r < RW; ++r) {
+            if (lane == 0) e[r] = N[r][0];
+            if (lane == 31) e[RW + r] = N[r][kC - 1];
         }
     };
 
-    // ---- step 0: the first plane is final as loaded --------------------------
+    float PA[RW][kC], IA[RW][kC], PB[RW][kC], IB[RW][kC];
+
+    // ---- step 0: the first plane is final as loaded ----------------------------
     {
-        mbar_wait(&full[0], 0u);
-        const float* sdc = sd + wv * DBOX;
-        const float* sic = si + wv * IBOX;
-        float N[RW][kC];
+        mbar_wait(&c.full[0], 0u);
 #pragma unroll
         for (int r = 0; r < RW; ++r) {
-            const float4 d4 = *reinterpret_cast<const float4*>(sdc + (r0 + r) * kWV + kC * lane);
-            N[r][0] = d4.x; N[r][1] = d4.y; N[r][2] = d4.z; N[r][3] = d4.w;
+            const float4 d4 =
+                *reinterpret_cast<const float4*>(sd_base + (r0 + r) * kWV + kC * lane);
+            PA[r][0] = d4.x; PA[r][1] = d4.y; PA[r][2] = d4.z; PA[r][3] = d4.w;
             if (kI) {
-                const float4 i4 = *reinterpret_cast<const float4*>(sic + (r0 + r + 1) * kIW + 4 +
-                                                                   kC * lane);
-                IP[r][0] = i4.x; IP[r][1] = i4.y; IP[r][2] = i4.z; IP[r][3] = i4.w;
+                const float4 i4 = *reinterpret_cast<const float4*>(si_base + (r0 + r + 1) * kIW +
+                                                                   4 + kC * lane);
+                IA[r][0] = i4.x; IA[r][1] = i4.y; IA[r][2] = i4.z; IA[r][3] = i4.w;
             } else {
 #pragma unroll
-                for (int c = 0; c < kC; ++c) IP[r][c] = 0.0f;
+                for (int q = 0; q < kC; ++q) IA[r][q] = 0.0f;
             }
+            if (!FULL) {
 #pragma unroll
-            for (int c = 0; c < kC; ++c)
-                if (!(rowv[r] && colv[c])) N[r][c] = INF;
+                for (int q = 0; q < kC; ++q)
+                    if (!(rowv[r] && colv[q])) PA[r][q] = INF;
+            }
         }
-        publish(0, N);
-#pragma unroll
-        for (int r = 0; r < RW; ++r)
-#pragma unroll
-            for (int c = 0; c < kC; ++c) P[r][c] = N[r][c];
+        if (J > 0) publish(0, PA);
         consumer_sync(nthreads);
     }
 
     int slot = 0;
     uint32_t phase = 0;
-    for (int j = 1; j <= J; ++j) {
-        const int pslot = slot;  // previous plane's slot
+    const float* sd_cur = sd_base;
+    const float* si_cur = si_base;
+
+    // One relaxation step: plane j from the previous plane (Pin, Iin) into (Pout, Iout).
+    auto step = [&](int j, const float (&Pin)[RW][kC], const float (&Iin)[RW][kC],
+                    float (&Pout)[RW][kC], float (&Iout)[RW][kC]) {
+        const int pslot = slot;
+        const float* sip = si_cur;  // previous plane's I box
         if (++slot == NST) {
             slot = 0;
             phase ^= 1u;
+            sd_cur = sd_base;
+            si_cur = si_base;
+        } else {
+            sd_cur += SD_STRIDE;
+            si_cur += SI_STRIDE;
         }
         const int par = (j - 1) & 1;
-        const long long hoff = par * 2ll * VW;
-        const uint32_t want = p.tag_base + static_cast<uint32_t>(j - 1);
+        const uint32_t want = tag_base + static_cast<uint32_t>(j - 1);
+        const unsigned long long* hup = up0 + par * 2ll * VW;
+        const unsigned long long* hdn = dn0 + par * 2ll * VW;
         unsigned long long hu[6], hd[6];  // [0] = v-1, [1..4] own, [5] = v+4
-        if (has_up) load_halo_row(up_base + hoff, has_left, has_right, hu);
-        if (has_dn) load_halo_row(dn_base + hoff, has_left, has_right, hd);
+        auto load_row = [&](const unsigned long long* q, unsigned long long (&h)[6]) {
+            h[0] = ld_tagged(q + dl);
+            ld_tagged2(q, h[1], h[2]);
+            ld_tagged2(q + 2, h[3], h[4]);
+            h[5] = ld_tagged(q + dr);
+        };
+        if (TOP && has_up) load_row(hup, hu);
+        if (BOT && has_dn) load_row(hdn, hd);
 
-        mbar_wait(&full[slot], phase);
-        const float* sdc = sd + (slot * nwv + wv) * DBOX;
-        const float* sic = si + (slot * nwv + wv) * IBOX;
-        const float* sip = si + (pslot * nwv + wv) * IBOX;  // previous plane's I box
+        mbar_wait(&c.full[slot], phase);
         float dold[RW][kC], ic[RW][kC];
 #pragma unroll
         for (int r = 0; r < RW; ++r) {
-            const float4 d4 = *reinterpret_cast<const float4*>(sdc + (r0 + r) * kWV + kC * lane);
+            const float4 d4 =
+                *reinterpret_cast<const float4*>(sd_cur + (r0 + r) * kWV + kC * lane);
             dold[r][0] = d4.x; dold[r][1] = d4.y; dold[r][2] = d4.z; dold[r][3] = d4.w;
             if (kI) {
-                const float4 i4 = *reinterpret_cast<const float4*>(sic + (r0 + r + 1) * kIW + 4 +
-                                                                   kC * lane);
+                const float4 i4 = *reinterpret_cast<const float4*>(si_cur + (r0 + r + 1) * kIW +
+                                                                   4 + kC * lane);
                 ic[r][0] = i4.x; ic[r][1] = i4.y; ic[r][2] = i4.z; ic[r][3] = i4.w;
             } else {
 #pragma unroll
-                for (int c = 0; c < kC; ++c) ic[r][c] = 0.0f;
+                for (int q = 0; q < kC; ++q) ic[r][q] = 0.0f;
             }
         }
 
-        const float* rows_prev = rows + par * NWU * 2 * VW;
-        const float* edge_prev = edge + par * NWU * nwv * 2 * RW;
+        const float* rows_prev = c.rows + par * RPAR;
+        const float* edge_prev = c.edge + par * EPAR;
         Acc<KIND, F64> acc[RW][kC];
 #pragma unroll
         for (int r = 0; r < RW; ++r)
 #pragma unroll
-            for (int c = 0; c < kC; ++c) acc[r][c].init(dold[r][c]);
+            for (int q = 0; q < kC; ++q) acc[r][q].init(dold[r][q]);
 
-        // Intensity window of previous-plane strip row `sr` (box row sr+1).
         auto i_window = [&](int sr, float (&iw)[6]) {
             if (kI) {
                 const float* rp = sip + (sr + 1) * kIW;
@@ -422,22 +394,21 @@ __global__ void __launch_bounds__((MW * NWU + 1) * 32, 1)
 #pragma unroll
         for (int k = 0; k < RW; ++k) {
             float pw[6], iw[6];
-            const float eL = wv > 0 ? edge_prev[((wu * nwv + wv - 1) * 2 + 1) * RW + k] : INF;
-            const float eR = wv + 1 < nwv ? edge_prev[((wu * nwv + wv + 1) * 2 + 0) * RW + k] : INF;
-            make_window(P[k], eL, eR, lane, pw);
+            const float eL = wl ? edge_prev[eoffL + k] : INF;
+            const float eR = wr ? edge_prev[eoffR + k] : INF;
+            make_window(Pin[k], eL, eR, lane, pw);
             if (kI) {
                 const float* rp = sip + (r0 + k + 1) * kIW;
-                make_window(IP[k], rp[3], rp[4 + kWV], lane, iw);
+                make_window(Iin[k], rp[3], rp[4 + kWV], lane, iw);
             } else {
 #pragma unroll
                 for (int i = 0; i < 6; ++i) iw[i] = 0.0f;
             }
-            // prev row k feeds output rows k-1 (du=+1), k (du=0), k+1 (du=-1)
             if (k - 1 >= 0) relax_row<KIND, F64>(acc[k - 1], pw, iw, ic[k - 1], +1, p);
             relax_row<KIND, F64>(acc[k], pw, iw, ic[k], 0, p);
             if (k + 1 < RW) relax_row<KIND, F64>(acc[k + 1], pw, iw, ic[k + 1], -1, p);
         }
-        if (!top_warp) {
+        if (!TOP) {
             const float* rp = rows_prev + ((wu - 1) * 2 + 1) * VW;  // last row of warp row wu-1
             const float4 q4 = *reinterpret_cast<const float4*>(rp + vl);
             const float c4[kC] = {q4.x, q4.y, q4.z, q4.w};
@@ -446,7 +417,7 @@ __global__ void __launch_bounds__((MW * NWU + 1) * 32, 1)
             i_window(r0 - 1, iw);
             relax_row<KIND, F64>(acc[0], pw, iw, ic[0], -1, p);
         }
-        if (!bot_warp) {
+        if (!BOT) {
             const float* rp = rows_prev + ((wu + 1) * 2 + 0) * VW;  // first row of warp row wu+1
             const float4 q4 = *reinterpret_cast<const float4*>(rp + vl);
             const float c4[kC] = {q4.x, q4.y, q4.z, q4.w};
@@ -457,99 +428,195 @@ __global__ void __launch_bounds__((MW * NWU + 1) * 32, 1)
         }
 
         // ---- phase B: rows above / below the strip (tagged halo) -------------
-        if (top_warp || bot_warp) {
+        if (TOP || BOT) {
             auto fresh = [&](const unsigned long long (&h)[6]) {
                 bool ok = true;
 #pragma unroll
-                for (int i = 0; i < 6; ++i) {
-                    const bool need = (i > 0 && i < 5) || (i == 0 ? has_left : has_right);
-                    ok = ok && (!need || tag_of(h[i]) == want);
-                }
+                for (int i = 0; i < 6; ++i) ok = ok && tag_of(h[i]) == want;
                 return ok;
             };
             long long spins = 0;
             while (true) {
-                const bool ok_u = !has_up || fresh(hu);
-                const bool ok_d = !has_dn || fresh(hd);
+                const bool ok_u = !(TOP && has_up) || fresh(hu);
+                const bool ok_d = !(BOT && has_dn) || fresh(hd);
                 if (__all_sync(kFull, ok_u && ok_d)) break;
-                if (!ok_u) load_halo_row(up_base + hoff, has_left, has_right, hu);
-                if (!ok_d) load_halo_row(dn_base + hoff, has_left, has_right, hd);
+                if (!ok_u) load_row(hup, hu);
+                if (!ok_d) load_row(hdn, hd);
                 if (++spins > kSpinLimit) __trap();
             }
-            if (top_warp) {
+            if (TOP) {
                 float pw[6], iw[6];
 #pragma unroll
-                for (int i = 0; i < 6; ++i) {
-                    const bool need = (i > 0 && i < 5) || (i == 0 ? has_left : has_right);
-                    pw[i] = (has_up && need) ? val_of(hu[i]) : INF;
-                }
+                for (int i = 0; i < 6; ++i) pw[i] = has_up ? val_of(hu[i]) : INF;
+                if (!has_left) pw[0] = INF;
+                if (!has_right) pw[5] = INF;
                 i_window(-1, iw);
                 relax_row<KIND, F64>(acc[0], pw, iw, ic[0], -1, p);
             }
-            if (bot_warp) {
+            if (BOT) {
                 float pw[6], iw[6];
 #pragma unroll
-                for (int i = 0; i < 6; ++i) {
-                    const bool need = (i > 0 && i < 5) || (i == 0 ? has_left : has_right);
-                    pw[i] = (has_dn && need) ? val_of(hd[i]) : INF;
-                }
+                for (int i = 0; i < 6; ++i) pw[i] = has_dn ? val_of(hd[i]) : INF;
+                if (!has_left) pw[0] = INF;
+                if (!has_right) pw[5] = INF;
                 i_window(R, iw);
                 relax_row<KIND, F64>(acc[RW - 1], pw, iw, ic[RW - 1], +1, p);
             }
         }
-
-        float N[RW][kC];
-        if (all_valid) {
-#pragma unroll
-            for (int r = 0; r < RW; ++r)
-#pragma unroll
-                for (int c = 0; c < kC; ++c) N[r][c] = acc[r][c].final(p);
-        } else {
-#pragma unroll
-            for (int r = 0; r < RW; ++r)
-#pragma unroll
-                for (int c = 0; c < kC; ++c)
-                    N[r][c] = (rowv[r] && colv[c]) ? acc[r][c].final(p) : INF;
-        }
-
-        publish(j, N);
-
-        // ---- store the relaxed plane ------------------------------------------
-        const long long soff = static_cast<long long>(plane_of(j)) * p.ss;
-        if (all_valid) {
-#pragma unroll
-            for (int r = 0; r < RW; ++r)
-                *reinterpret_cast<float4*>(outp[r] + soff) =
-                    make_float4(N[r][0], N[r][1], N[r][2], N[r][3]);
-        } else {
-#pragma unroll
-            for (int r = 0; r < RW; ++r) {
-                if (!rowv[r]) continue;
-                float* q = outp[r] + soff;
-                if (colv[kC - 1]) {
-                    *reinterpret_cast<float4*>(q) = make_float4(N[r][0], N[r][1], N[r][2], N[r][3]);
-                } else {
-#pragma unroll
-                    for (int c = 0; c < kC; ++c)
-                        if (colv[c]) q[c] = N[r][c];
-                }
-            }
-        }
-        if (p.fence_turn && j <= n1) fence_proxy_async_global();
-
+        // The previous plane's slot is no longer read by this warp.
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[pslot]);  // previous plane's slot fully consumed
-        consumer_sync(nthreads);
-        if (tid == 0) st_release_cta(progress, j);
+        if (lane == 0) mbar_arrive(&c.empty[pslot]);
 
 #pragma unroll
         for (int r = 0; r < RW; ++r)
 #pragma unroll
-            for (int c = 0; c < kC; ++c) {
-                P[r][c] = N[r][c];
-                IP[r][c] = ic[r][c];
+            for (int q = 0; q < kC; ++q) {
+                Pout[r][q] = acc[r][q].final(p);
+                if (!FULL && !(rowv[r] && colv[q])) Pout[r][q] = INF;
+                Iout[r][q] = ic[r][q];
             }
+
+        if (j < J) publish(j, Pout);
+
+        // ---- store the relaxed plane ------------------------------------------
+        if (j == n1 + 1) dsoff = -dsoff;  // the backward pass walks back
+        outp += dsoff;
+#pragma unroll
+        for (int r = 0; r < RW; ++r) {
+            float* q = outp + r * su;
+            if (FULL) {
+                *reinterpret_cast<float4*>(q) =
+                    make_float4(Pout[r][0], Pout[r][1], Pout[r][2], Pout[r][3]);
+            } else if (rowv[r]) {
+                if (colv[kC - 1]) {
+                    *reinterpret_cast<float4*>(q) =
+                        make_float4(Pout[r][0], Pout[r][1], Pout[r][2], Pout[r][3]);
+                } else {
+#pragma unroll
+                    for (int q2 = 0; q2 < kC; ++q2)
+                        if (colv[q2]) q[q2] = Pout[r][q2];
+                }
+            }
+        }
+        // Backward planes are read back through TMA (async proxy): order this
+        // thread's stores before them.  A fence covers all earlier stores too,
+        // so only the last forward steps (those the producer may fetch before
+        // the turn completes) need one.
+        const bool near_turn = turn_fence && j <= n1 && j + NST >= n1;
+        if (near_turn) fence_proxy_async_global();
+
+        consumer_sync(nthreads);
+        if (tid == 0 && near_turn) st_release_cta(c.progress, j);
+    };
+
+    int j = 1;
+    for (; j + 1 <= J; j += 2) {
+        step(j, PA, IA, PB, IB);
+        step(j + 1, PB, IB, PA, IA);
     }
+    if (j <= J) step(j, PA, IA, PB, IB);
+}
+
+// Warp-specialised persistent sweep: warps [0, NWU*nwv) relax the strip, the
+// last warp is the TMA producer.  Slot j % NST carries plane p(j); it is
+// released ("empty") by every consumer warp during step j+1, which reads it as
+// the previous plane's intensities.
+template <int KIND, bool F64, int RW, int NWU, int NST, int MW>
+__global__ void __launch_bounds__((MW * NWU + 1) * 32, 1)
+    sweep_kernel(const __grid_constant__ CUtensorMap tm_d, const __grid_constant__ CUtensorMap tm_i,
+                 const __grid_constant__ SweepParams p) {
+    using L = Layout<RW, NWU, NST>;
+    constexpr int DBOX = L::DBOX, IBOX = L::IBOX;
+    constexpr bool kI = KIND != kSpatial;  // Spatial never reads intensities
+    constexpr uint32_t TXW = static_cast<uint32_t>(kI ? DBOX * 4 + L::IBYTES : DBOX * 4);
+
+    const int nwv = p.nwv;
+    const int ncw = NWU * nwv;  // consumer warps
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    Ctx<RW, NWU, NST> c;
+    c.sd = reinterpret_cast<float*>(smem_raw);
+    c.si = c.sd + NST * nwv * DBOX;
+    c.rows = c.si + NST * nwv * IBOX;
+    c.edge = c.rows + 2 * NWU * 2 * nwv * kWV;
+    c.full = reinterpret_cast<uint64_t*>(c.edge + 2 * NWU * nwv * 2 * RW);
+    c.empty = c.full + NST;
+    c.progress = reinterpret_cast<int*>(c.empty + NST);
+    c.nwv = nwv;
+    c.g = blockIdx.x;
+    c.b = c.g / p.ntu;
+    c.tu = c.g - c.b * p.ntu;
+    c.u0 = c.tu * L::R;
+    c.n1 = p.ns - 1;
+    c.J = p.npass * c.n1;
+    c.VW = nwv * kWV;
+
+    if (tid == 0) {
+        for (int s = 0; s < NST; ++s) {
+            mbar_init(&c.full[s], 1);
+            mbar_init(&c.empty[s], ncw);
+        }
+        *c.progress = -1;
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    // ======================= producer warp ==================================
+    if (w == ncw) {
+        if (lane == 0) {
+            tma_prefetch_desc(&tm_d);
+            if (kI) tma_prefetch_desc(&tm_i);
+            for (int j = 0; j <= c.J; ++j) {
+                const int slot = j % NST, k = j / NST;
+                if (k > 0) mbar_wait(&c.empty[slot], static_cast<uint32_t>((k - 1) & 1));
+                // A backward-pass plane is the forward pass's output of step 2*n1 - j.
+                if (j > c.n1) {
+                    const int jf = 2 * c.n1 - j;
+                    while (ld_acquire_cta(c.progress) < jf) {
+                    }
+                }
+                const int s = plane_of(p, c, j);
+                mbar_arrive_expect_tx(&c.full[slot], TXW * nwv);
+                for (int cb = 0; cb < nwv; ++cb) {
+                    float* dd = c.sd + (slot * nwv + cb) * DBOX;
+                    float* di = c.si + (slot * nwv + cb) * IBOX;
+                    const int v0 = cb * kWV;
+                    if (p.tma_sweep_dim == 2) {
+                        tma_load_4d(dd, &tm_d, &c.full[slot], v0, c.u0, s, c.b);
+                        if (kI) tma_load_4d(di, &tm_i, &c.full[slot], v0 - 4, c.u0 - 1, s, c.b);
+                    } else {
+                        tma_load_4d(dd, &tm_d, &c.full[slot], v0, s, c.u0, c.b);
+                        if (kI) tma_load_4d(di, &tm_i, &c.full[slot], v0 - 4, s, c.u0 - 1, c.b);
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    // ======================= consumer warps =================================
+    const int wu = w / nwv, wv = w - wu * nwv;
+    const int vl = wv * kWV + kC * lane;
+    const bool full =
+        __all_sync(kFull, (c.u0 + wu * RW + RW <= p.nu) && (vl + kC <= p.nv));
+    const bool top = wu == 0, bot = wu == NWU - 1;
+#define GD_ROLE(T, B)                                                                      \
+    if (top == T && bot == B) {                                                            \
+        if (full)                                                                          \
+            consumer_loop<KIND, F64, RW, NWU, NST, T, B, true>(p, c, wu, wv, lane);        \
+        else                                                                               \
+            consumer_loop<KIND, F64, RW, NWU, NST, T, B, false>(p, c, wu, wv, lane);       \
+        return;                                                                            \
+    }
+    if (NWU == 1) {
+        GD_ROLE(true, true)
+    } else {
+        GD_ROLE(true, false)
+        GD_ROLE(false, true)
+        if (NWU > 2) GD_ROLE(false, false)
+    }
+#undef GD_ROLE
 }
 
 template <int KIND, bool F64, int RW, int NWU, int NST, int MW>
@@ -585,7 +652,7 @@ int coresident(int nwv) {
     return per_sm * sms;
 }
 
-constexpr int kNST = 4;
+constexpr int kNST = 6;
 
 // Strip shapes (rows per warp RW, warp rows NWU, max warp columns MW): narrow
 // planes (<= 512 columns) run 2 warp rows of 2 rows (R = 4, 2 warps per

@@ -18,15 +18,18 @@ ap.add_argument("--shape", default="512,512,512")
 ap.add_argument("--spacing", default="1,1,2.5")
 ap.add_argument("--iters", type=int, default=4)
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--batch", type=int, default=1)
 a = ap.parse_args()
 shape = tuple(int(x) for x in a.shape.split(","))
+full = ((a.batch,) + shape) if a.batch > 1 else shape
 spacing = tuple(float(x) for x in a.spacing.split(","))
-img = torch.empty(shape, dtype=torch.float32, device="cuda")
+img = torch.empty(full, dtype=torch.float32, device="cuda")
 gd.device.fill_splitmix(img, 0x67656F64697374 ^ (3 << 32) ^ shape[-1])
-mask = torch.ones(shape, dtype=torch.float32, device="cuda")
-mask[tuple(s // 2 for s in shape)] = 0.0
+mask = torch.ones(full, dtype=torch.float32, device="cuda")
+mask[tuple(s // 2 for s in full)] = 0.0
 out = torch.empty_like(img)
 for _ in range(a.reps):
-    gd.device.generalized_geodesic(img, mask, out, spacing, a.lam, 1e10, a.iters)
+    gd.device.generalized_geodesic(img, mask, out, spacing, a.lam, 1e10, a.iters,
+                                   batch=a.batch if a.batch > 1 else None)
 torch.cuda.synchronize()
 print("ok", float(out.max().item()))
