@@ -26,7 +26,7 @@ __all__ = [
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libgeodist_b200.so")
+LIB_PATH = os.environ.get("GEODIST_LIB") or os.path.join(HERE, "lib", "libgeodist_b200.so")
 
 GD_OK, GD_INVALID_ARGUMENT, GD_EMPTY_SEEDS, GD_CUDA_ERROR, GD_UNSUPPORTED = range(5)
 GD_MEM_HOST, GD_MEM_DEVICE = 0, 1

@@ -8,6 +8,8 @@
 #include <atomic>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -113,7 +115,7 @@ struct StreamCtx {
     Buf halo;
     size_t halo_bytes_zeroed = 0;
     uint32_t tag = 1;  // 0 never matches: freshly zeroed halo words are stale
-    Buf dT, iT, padI, padD, tmp, small;
+    Buf dT, iT, padI, padD, tmp, small, trace;
 };
 
 struct DeviceCtx {
@@ -354,11 +356,43 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
         p.halo = sc.halo.as<unsigned long long>();
         p.tag_base = sc.tag;
         sc.tag += static_cast<uint32_t>(J + 1);
+        // Diagnostic cycle counters: only a -DGD_SWEEP_TRACE build writes them.
+        static const bool trace_on = std::getenv("GEODIST_SWEEP_TRACE") != nullptr;
+        const size_t trace_n = static_cast<size_t>(nvol) * per_vol * 64 * 8;
+        if (trace_on) {
+            GD_ST(sc.trace.ensure(trace_n * sizeof(long long)));
+            GD_CK(cudaMemsetAsync(sc.trace.p, 0, trace_n * sizeof(long long), s));
+            p.trace = sc.trace.as<long long>();
+        }
         {
             const double bytes = static_cast<double>(nvol) * g.voxels() * npass *
                                  (kind == kSpatial ? 8.0 : 12.0);
             ProfScope ps(kProfSweep, bytes, s);
             GD_CK(launch_sweep(kind, f64, R, tm_d, tm_i, p, s));
+        }
+        if (trace_on) {
+            std::vector<long long> h(trace_n);
+            GD_CK(cudaMemcpyAsync(h.data(), sc.trace.p, trace_n * sizeof(long long),
+                                  cudaMemcpyDeviceToHost, s));
+            GD_CK(cudaStreamSynchronize(s));
+            const int nw = nwv * (R == 1 ? 1 : (R == 2 ? 1 : 2));
+            for (int w = 0; w < nw; ++w) {
+                double acc[6] = {0, 0, 0, 0, 0, 0};
+                long long n = 0;
+                for (long long cta = 0; cta < nvol * per_vol; ++cta) {
+                    const long long* o = &h[(cta * 64 + w) * 8];
+                    if (o[5] == 0) continue;
+                    for (int k = 0; k < 6; ++k) acc[k] += o[k];
+                    ++n;
+                }
+                if (!n) continue;
+                const double steps = acc[5] / n;
+                std::fprintf(stderr,
+                             "trace axis=%d warp=%d: cycles/step total %.0f tma %.0f spin %.0f "
+                             "barrier %.0f reloads/step %.2f (ctas %lld)\n",
+                             axis, w, acc[4] / n / steps, acc[0] / n / steps, acc[1] / n / steps,
+                             acc[2] / n / steps, acc[3] / n / steps, n);
+            }
         }
         ++g_launches;
         if (st) ++st->kernel_launches;

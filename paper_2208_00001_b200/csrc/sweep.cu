@@ -102,6 +102,20 @@ struct Acc<kSpatial, F64> {
 // instructions per voxel); the scalar FADD with an |operand| is cheaper.
 constexpr bool kPackedIntensity = false;
 
+// Second halo poll issued mid-step (alternating spin).  Measured slower on
+// B200 (1.48 vs 1.24 us/step at 512^2): the extra loads and registers cost more
+// than the earlier detection gains.
+constexpr bool kDualPoll = false;
+
+// Cycle counters for diagnosis (built only with -DGD_SWEEP_TRACE).
+#ifdef GD_SWEEP_TRACE
+#define GD_T0(v) const long long v = clock64()
+#define GD_TADD(slot, v) trc[slot] += clock64() - (v)
+#else
+#define GD_T0(v)
+#define GD_TADD(slot, v)
+#endif
+
 // The 3-column windows of one previous-plane row for a lane's 4 columns:
 // pw/iw[0] = column v-1, [1..4] = own columns, [5] = column v+4.
 template <int KIND, bool F64>
@@ -263,7 +277,7 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
     const float* const si_base = c.si + wv * IBOX;
     const int SD_STRIDE = nwv * DBOX, SI_STRIDE = nwv * IBOX;
 
-    auto publish = [&](int j, const float (&N)[RW][kC]) {
+    auto publish_halo = [&](int j, const float (&N)[RW][kC]) {
         const int par = j & 1;
         const uint32_t tag = tag_base + static_cast<uint32_t>(j);
         unsigned long long* q = self0 + par * 2ll * VW;
@@ -275,6 +289,9 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
             st_tagged2(q + VW, N[RW - 1][0], N[RW - 1][1], tag);
             st_tagged2(q + VW + 2, N[RW - 1][2], N[RW - 1][3], tag);
         }
+    };
+    auto publish_smem = [&](int j, const float (&N)[RW][kC]) {
+        const int par = j & 1;
         if (NWU > 1) {
             float* rw_ = c.rows + par * RPAR + wu * 2 * VW;
             if (!TOP)
@@ -293,6 +310,10 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
     };
 
     float PA[RW][kC], IA[RW][kC], PB[RW][kC], IB[RW][kC];
+#ifdef GD_SWEEP_TRACE
+    long long trc[6] = {0, 0, 0, 0, 0, 0};  // tma wait, halo spin, barrier, reloads, total, steps
+    const long long t_begin = clock64();
+#endif
 
     // ---- step 0: the first plane is final as loaded ----------------------------
     {
@@ -316,7 +337,10 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
                     if (!(rowv[r] && colv[q])) PA[r][q] = INF;
             }
         }
-        if (J > 0) publish(0, PA);
+        if (J > 0) {
+            publish_halo(0, PA);
+            publish_smem(0, PA);
+        }
         consumer_sync(nthreads);
     }
 
@@ -343,17 +367,22 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
         const uint32_t want = tag_base + static_cast<uint32_t>(j - 1);
         const unsigned long long* hup = up0 + par * 2ll * VW;
         const unsigned long long* hdn = dn0 + par * 2ll * VW;
-        unsigned long long hu[6], hd[6];  // [0] = v-1, [1..4] own, [5] = v+4
+        // Two polls of each halo window are kept in flight: A at the top of the
+        // step, B after the strip's own rows are relaxed; the spin alternates
+        // between them so a fresh word is seen within about half a round trip.
+        unsigned long long huA[6], hdA[6], huB[6], hdB[6];  // [0] = v-1, [1..4] own, [5] = v+4
         auto load_row = [&](const unsigned long long* q, unsigned long long (&h)[6]) {
             h[0] = ld_tagged(q + dl);
             ld_tagged2(q, h[1], h[2]);
             ld_tagged2(q + 2, h[3], h[4]);
             h[5] = ld_tagged(q + dr);
         };
-        if (TOP && has_up) load_row(hup, hu);
-        if (BOT && has_dn) load_row(hdn, hd);
+        if (TOP && has_up) load_row(hup, huA);
+        if (BOT && has_dn) load_row(hdn, hdA);
 
+        GD_T0(t_tma);
         mbar_wait(&c.full[slot], phase);
+        GD_TADD(0, t_tma);
         float dold[RW][kC], ic[RW][kC];
 #pragma unroll
         for (int r = 0; r < RW; ++r) {
@@ -408,6 +437,10 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
             relax_row<KIND, F64>(acc[k], pw, iw, ic[k], 0, p);
             if (k + 1 < RW) relax_row<KIND, F64>(acc[k + 1], pw, iw, ic[k + 1], -1, p);
         }
+        if (kDualPoll) {
+            if (TOP && has_up) load_row(hup, huB);
+            if (BOT && has_dn) load_row(hdn, hdB);
+        }
         if (!TOP) {
             const float* rp = rows_prev + ((wu - 1) * 2 + 1) * VW;  // last row of warp row wu-1
             const float4 q4 = *reinterpret_cast<const float4*>(rp + vl);
@@ -436,13 +469,33 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
                 return ok;
             };
             long long spins = 0;
+            GD_T0(t_spin);
+            bool useB = false;
             while (true) {
-                const bool ok_u = !(TOP && has_up) || fresh(hu);
-                const bool ok_d = !(BOT && has_dn) || fresh(hd);
-                if (__all_sync(kFull, ok_u && ok_d)) break;
-                if (!ok_u) load_row(hup, hu);
-                if (!ok_d) load_row(hdn, hd);
+                const bool ok = useB ? ((!(TOP && has_up) || fresh(huB)) &&
+                                        (!(BOT && has_dn) || fresh(hdB)))
+                                     : ((!(TOP && has_up) || fresh(huA)) &&
+                                        (!(BOT && has_dn) || fresh(hdA)));
+                if (__all_sync(kFull, ok)) break;
+                if (useB) {
+                    if (TOP && has_up) load_row(hup, huB);
+                    if (BOT && has_dn) load_row(hdn, hdB);
+                } else {
+                    if (TOP && has_up) load_row(hup, huA);
+                    if (BOT && has_dn) load_row(hdn, hdA);
+                }
+                if (kDualPoll) useB = !useB;
                 if (++spins > kSpinLimit) __trap();
+            }
+            GD_TADD(1, t_spin);
+#ifdef GD_SWEEP_TRACE
+            trc[3] += spins;
+#endif
+            unsigned long long hu[6], hd[6];
+#pragma unroll
+            for (int i = 0; i < 6; ++i) {
+                hu[i] = useB ? huB[i] : huA[i];
+                hd[i] = useB ? hdB[i] : hdA[i];
             }
             if (TOP) {
                 float pw[6], iw[6];
@@ -467,16 +520,22 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
         __syncwarp();
         if (lane == 0) mbar_arrive(&c.empty[pslot]);
 
-#pragma unroll
-        for (int r = 0; r < RW; ++r)
+        auto fin = [&](int r) {
 #pragma unroll
             for (int q = 0; q < kC; ++q) {
                 Pout[r][q] = acc[r][q].final(p);
                 if (!FULL && !(rowv[r] && colv[q])) Pout[r][q] = INF;
                 Iout[r][q] = ic[r][q];
             }
-
-        if (j < J) publish(j, Pout);
+        };
+        // Border rows first: they are the neighbours' critical path.
+        if (TOP) fin(0);
+        if (BOT && (RW > 1 || !TOP)) fin(RW - 1);
+        if (j < J) publish_halo(j, Pout);
+#pragma unroll
+        for (int r = 0; r < RW; ++r)
+            if (!((TOP && r == 0) || (BOT && r == RW - 1))) fin(r);
+        if (j < J) publish_smem(j, Pout);
 
         // ---- store the relaxed plane ------------------------------------------
         if (j == n1 + 1) dsoff = -dsoff;  // the backward pass walks back
@@ -505,7 +564,9 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
         const bool near_turn = turn_fence && j <= n1 && j + NST >= n1;
         if (near_turn) fence_proxy_async_global();
 
+        GD_T0(t_bar);
         consumer_sync(nthreads);
+        GD_TADD(2, t_bar);
         if (tid == 0 && near_turn) st_release_cta(c.progress, j);
     };
 
@@ -515,6 +576,14 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
         step(j + 1, PB, IB, PA, IA);
     }
     if (j <= J) step(j, PA, IA, PB, IB);
+#ifdef GD_SWEEP_TRACE
+    trc[4] = clock64() - t_begin;
+    trc[5] = J;
+    if (p.trace && lane == 0) {
+        long long* o = p.trace + (static_cast<long long>(c.g) * 64 + wu * nwv + wv) * 8;
+        for (int i = 0; i < 6; ++i) o[i] = trc[i];
+    }
+#endif
 }
 
 // Warp-specialised persistent sweep: warps [0, NWU*nwv) relax the strip, the

@@ -73,6 +73,7 @@ struct SweepParams {
     int fence_turn;           // emit fence.proxy.async on forward stores (npass == 2)
     uint32_t tag_base;
     unsigned long long* halo; // tagged halo words: [strip][parity][TOP|BOT][nwv*128]
+    long long* trace;         // optional per-warp cycle counters (null in production)
     // Neighbour coefficients indexed (du+1)*3 + (dv+1).
     double rho[9];
     double c0[9];
