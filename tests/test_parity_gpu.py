@@ -192,3 +192,28 @@ def test_invalid_arguments(gd):
         gd.parallel_scan(img, img, None, 1.5, 1)
     with pytest.raises(gd.InvalidArgument):
         gd.gsf(img, img, None, 1.0, 1e10, 2, -0.5)
+
+
+# ---- committed golden vectors from the unmodified reference -----------------
+import glob  # noqa: E402
+import os  # noqa: E402
+
+_GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
+
+
+@pytest.mark.parametrize("path", _GOLDEN, ids=[os.path.basename(p) for p in _GOLDEN])
+def test_cuda_matches_golden(gd, path):
+    from tests.test_oracle import run_fixture
+    f = np.load(path)
+    lam = float(f["lam"])
+    got = run_fixture(gd, f)
+    if lam in (0.0, 1.0) or str(f["kind"]) == "gsf":
+        assert bitwise_equal(got, f["out"]), parity(got, f["out"])
+    else:
+        ok, *_ = parity(got, f["out"])
+        assert ok
+        gd.set_exact_blend(True)
+        try:
+            assert bitwise_equal(run_fixture(gd, f), f["out"])
+        finally:
+            gd.set_exact_blend(False)
