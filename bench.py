@@ -68,31 +68,41 @@ def peak_hbm():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons, sampled from before the warm-up; the
+    summary keeps only the samples inside the timed window (mark_start/mark_end)."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    FIELDS = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpus):
         self.gpus = gpus
         self.proc = None
+        self.t0 = self.t1 = None
         self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
 
-    def __enter__(self):
+    def start(self):
         os.makedirs(os.path.dirname(self.path), exist_ok=True)
         try:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100", "-i", ",".join(str(g) for g in self.gpus)],
+                 "-lms", "50", "-i", ",".join(str(g) for g in self.gpus)],
                 stdout=self.fh, stderr=subprocess.DEVNULL)
+            time.sleep(0.5)  # let the sampler come up before the timed region
         except Exception:
             self.proc = None
         return self
 
-    def __exit__(self, *a):
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+
+    def stop(self):
         if self.proc:
+            time.sleep(0.1)
             self.proc.terminate()
             self.proc.wait()
             self.fh.close()
@@ -100,23 +110,30 @@ class ClockSampler:
     def summary(self):
         if not self.proc:
             return None
-        sm, mx, reasons = [], [], set()
+        import datetime
+        sm, mx, reasons, n_all = [], [], set(), 0
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         with open(self.path) as f:
             for line in f:
                 p = [x.strip() for x in line.split(",")]
-                if len(p) < 9:
+                if len(p) < 10:
                     continue
+                n_all += 1
                 try:
-                    sm.append(float(p[1]))
-                    mx.append(float(p[2]))
+                    ts = datetime.datetime.strptime(p[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                    s, m = float(p[2]), float(p[3])
                 except ValueError:
                     continue
-                for n, v in zip(names, p[5:9]):
+                if self.t0 is not None and not (self.t0 - 0.05 <= ts <= self.t1 + 0.05):
+                    continue
+                sm.append(s)
+                mx.append(m)
+                for n, v in zip(names, p[6:10]):
                     if v.lower() == "active":
                         reasons.add(n)
         if not sm:
-            return None
+            return {"sm_mhz": None, "sm_max_mhz": None, "samples": 0, "reasons": [],
+                    "note": f"no sample inside the timed window ({n_all} total)"}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "samples": len(sm),
                 "reasons": sorted(reasons)}
 
@@ -218,6 +235,9 @@ def main():
     def step():
         gd.device.generalized_geodesic(img, mask, out, SPACING, args.lam, NU, ITERS)
 
+    clk = ClockSampler(list(range(max(world, 1)))) if rank == 0 else None
+    if clk:
+        clk.start()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -227,15 +247,18 @@ def main():
     gd.profile_read(reset=True)
     gd.profile_enable(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(list(range(max(world, 1)))) as clk:
-        torch.cuda.synchronize()
-        barrier()
-        e0.record()
-        for _ in range(args.steps):
-            step()
-        e1.record()
-        torch.cuda.synchronize()
-        barrier()
+    torch.cuda.synchronize()
+    barrier()
+    if clk:
+        clk.mark_start()
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    if clk:
+        clk.mark_end()
+    barrier()
     gd.profile_enable(False)
     prof = gd.profile_read(reset=True)
     launches = gd.kernel_launches() - n0
@@ -338,7 +361,10 @@ def main():
             cpu_baseline = {"value": None, "unit": UNIT, "cores": os.cpu_count(),
                             "kind": "reference", "sample": "unavailable: oracle/_ref not built"}
 
-    clocks = clk.summary()
+    clocks = None
+    if clk:
+        clk.stop()
+        clocks = clk.summary()
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
