@@ -1,8 +1,8 @@
-// Element-wise and layout kernels around the sweep: soft-mask init, the
-// x-axis layout transposes, the per-image exactness check, GSF thresholds,
-// fixpoint change reduction, and the SplitMix64 synthetic-input generator.
-// All are HBM-bound streaming kernels: grid-stride loops, 16-byte accesses
-// where the layout allows, grid sized as a multiple of the SM count.
+// Element-wise and layout kernels around the sweep: soft-mask init (fused with
+// the mask-range / image-exactness check), the x-axis layout transposes, GSF
+// thresholds, fixpoint change reduction, and the SplitMix64 synthetic-input
+// generator.  All are HBM-bound streams: 16-byte accesses wherever the layout
+// allows, grid-stride loops, grids sized as a multiple of the SM count.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -14,128 +14,222 @@ namespace gdb {
 
 namespace {
 
-__device__ __forceinline__ long long vox_offset(const VolView& v, long long i, int& ok) {
-    // i enumerates logical voxels (b, z, y, x) densely.
-    ok = 1;
-    if (v.ys == v.W && v.zs == static_cast<long long>(v.H) * v.W &&
-        v.vol == static_cast<long long>(v.D) * v.zs)
-        return i;  // dense canonical layout
+__device__ __forceinline__ bool dense(const VolView& v) {
+    return v.ys == v.W && v.zs == static_cast<long long>(v.H) * v.W &&
+           v.vol == static_cast<long long>(v.D) * v.zs;
+}
+
+// i enumerates logical voxels (b, z, y, x) densely.
+__device__ __forceinline__ long long vox_offset(const VolView& v, long long i) {
+    if (dense(v)) return i;
     const long long x = i % v.W;
     long long t = i / v.W;
     const long long y = t % v.H;
     t /= v.H;
     const long long z = t % v.D;
     const long long b = t / v.D;
-    ok = 1;
     return b * v.vol + z * v.zs + y * v.ys + x;
 }
 
-__global__ void init_generalized_kernel(VolView m, VolView d, const float* mask, float* dist,
-                                        double nu, long long n) {
-    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        int ok;
-        const long long om = vox_offset(m, i, ok);
-        const long long od = vox_offset(d, i, ok);
-        // transforms.cpp:150-156: f32(min(nu * f64(M), f64(1e10)))
-        const double v = nu * static_cast<double>(mask[om]);
-        dist[od] = static_cast<float>(v < 1.0e10 ? v : 1.0e10);
-    }
-}
-
-// Transpose [b][z][y][x] (src view) -> [b][x][z][y] (dst view) or back.
-// 32x32 tiles over (y, x) per (b, z); reads and writes both coalesced.
-template <bool FWD>
-__global__ void transpose_kernel(VolView src_v, VolView dst_v, const float* src, float* dst) {
-    __shared__ float tile[32][33];
-    const int D = src_v.D, H = src_v.H, W = src_v.W;
-    for (int bz = blockIdx.z; bz < D * src_v.B; bz += gridDim.z) {
-    const int z = bz % D, b = bz / D;
-    const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
-    const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
-    if (FWD) {
-        // src [b][z][y][x] row pitch ys; dst [b][x][z][y]: element (x,z,y) at x*dst.zs + z*dst.ys + y
-        for (int k = ty; k < 32; k += 8) {
-            const int y = y0 + k, x = x0 + tx;
-            if (y < H && x < W)
-                tile[k][tx] = src[b * src_v.vol + z * src_v.zs + static_cast<long long>(y) * src_v.ys + x];
-        }
-        __syncthreads();
-        for (int k = ty; k < 32; k += 8) {
-            const int x = x0 + k, y = y0 + tx;
-            if (y < H && x < W)
-                dst[b * dst_v.vol + static_cast<long long>(x) * dst_v.zs + z * dst_v.ys + y] = tile[tx][k];
-        }
-    } else {
-        // src [b][x][z][y] -> dst [b][z][y][x]
-        for (int k = ty; k < 32; k += 8) {
-            const int x = x0 + k, y = y0 + tx;
-            if (y < H && x < W)
-                tile[k][tx] = src[b * src_v.vol + static_cast<long long>(x) * src_v.zs + z * src_v.ys + y];
-        }
-        __syncthreads();
-        for (int k = ty; k < 32; k += 8) {
-            const int y = y0 + k, x = x0 + tx;
-            if (y < H && x < W)
-                dst[b * dst_v.vol + z * dst_v.zs + static_cast<long long>(y) * dst_v.ys + x] = tile[tx][k];
-        }
-    }
-    __syncthreads();
-    }
-}
-
-// Image exactness: with x = m * 2^t (m odd), all pairwise differences are
-// exact in f32 when (max exponent) - (min t) <= 23 (same sign) / 22 (mixed).
-// Also flags masks outside [0, 1] (transforms.cpp:22-28).
-__global__ void image_check_kernel(VolView v, const float* img, const float* mask,
-                                   ImageCheck* out, long long n) {
-    int emax = -1000, tmin = 1000, pos = 0, neg = 0, bad_mask = 0, nonfinite = 0;
-    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        int ok;
-        const long long o = vox_offset(v, i, ok);
-        if (img) {
-            const float x = img[o];
-            const uint32_t u = __float_as_uint(x);
-            const int ebits = (u >> 23) & 0xff;
-            const uint32_t man = u & 0x7fffffu;
-            if (ebits == 0xff) {
-                nonfinite = 1;
-            } else if (ebits != 0 || man != 0) {
-                int e, t;
-                if (ebits == 0) {  // subnormal: value = man * 2^-149
-                    e = -149 + (31 - __clz(man));
-                    t = -149 + (__ffs(man) - 1);
-                } else {
-                    const uint32_t full = man | 0x800000u;
-                    e = ebits - 127;
-                    t = ebits - 150 + (__ffs(full) - 1);
-                }
-                emax = max(emax, e);
-                tmin = min(tmin, t);
-                if (u >> 31) neg = 1; else pos = 1;
+// Exponent statistics for the exactness test (see ImageCheck).
+struct ExpStats {
+    int emax = -1000, tmin = 1000, pos = 0, neg = 0, nonfinite = 0;
+    __device__ __forceinline__ void add(float x) {
+        const uint32_t u = __float_as_uint(x);
+        const int ebits = (u >> 23) & 0xff;
+        const uint32_t man = u & 0x7fffffu;
+        if (ebits == 0xff) {
+            nonfinite = 1;
+        } else if (ebits != 0 || man != 0) {
+            int e, t;
+            if (ebits == 0) {  // subnormal: value = man * 2^-149
+                e = -149 + (31 - __clz(man));
+                t = -149 + (__ffs(man) - 1);
+            } else {
+                e = ebits - 127;
+                t = ebits - 150 + (__ffs(man | 0x800000u) - 1);
             }
-        }
-        if (mask) {
-            const float m = mask[o];
-            if (!(m >= 0.0f && m <= 1.0f)) bad_mask = 1;
+            emax = max(emax, e);
+            tmin = min(tmin, t);
+            if (u >> 31) neg = 1; else pos = 1;
         }
     }
-    for (int s = 16; s > 0; s >>= 1) {
-        emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, s));
-        tmin = min(tmin, __shfl_xor_sync(0xffffffffu, tmin, s));
-        pos |= __shfl_xor_sync(0xffffffffu, pos, s);
-        neg |= __shfl_xor_sync(0xffffffffu, neg, s);
-        bad_mask |= __shfl_xor_sync(0xffffffffu, bad_mask, s);
-        nonfinite |= __shfl_xor_sync(0xffffffffu, nonfinite, s);
+};
+
+__device__ __forceinline__ void flush_check(const ExpStats& s, int bad_mask, ImageCheck* out) {
+    int emax = s.emax, tmin = s.tmin, pos = s.pos, neg = s.neg, nf = s.nonfinite, bm = bad_mask;
+    for (int o = 16; o > 0; o >>= 1) {
+        emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+        tmin = min(tmin, __shfl_xor_sync(0xffffffffu, tmin, o));
+        pos |= __shfl_xor_sync(0xffffffffu, pos, o);
+        neg |= __shfl_xor_sync(0xffffffffu, neg, o);
+        nf |= __shfl_xor_sync(0xffffffffu, nf, o);
+        bm |= __shfl_xor_sync(0xffffffffu, bm, o);
     }
     if ((threadIdx.x & 31) == 0) {
         atomicMax(&out->emax, emax);
         atomicMin(&out->tmin, tmin);
         if (pos) atomicOr(&out->pos, 1);
         if (neg) atomicOr(&out->neg, 1);
-        if (bad_mask) atomicOr(&out->bad_mask, 1);
-        if (nonfinite) atomicOr(&out->nonfinite, 1);
+        if (bm) atomicOr(&out->bad_mask, 1);
+        if (nf) atomicOr(&out->nonfinite, 1);
+    }
+}
+
+__device__ __forceinline__ float init_value(float m, double nu) {
+    // transforms.cpp:150-156: f32(min(nu * f64(M), f64(1e10)))
+    const double v = nu * static_cast<double>(m);
+    return static_cast<float>(v < 1.0e10 ? v : 1.0e10);
+}
+
+// Soft-mask init fused with the input checks: one pass over image + mask.
+// `img` may be null (no exactness check wanted).  `m` and `d` views may differ
+// (the distance may live in a padded working layout).
+__global__ void init_check_kernel(VolView mv, VolView dv, const float* img, const float* mask,
+                                  float* dist, double nu, ImageCheck* out, long long n) {
+    ExpStats st;
+    int bad = 0;
+    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    const long long t0 = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (dense(mv) && dense(dv) && (n & 3) == 0) {
+        const long long n4 = n >> 2;
+        for (long long i = t0; i < n4; i += stride) {
+            const float4 m = reinterpret_cast<const float4*>(mask)[i];
+            bad |= !(m.x >= 0.0f && m.x <= 1.0f) | !(m.y >= 0.0f && m.y <= 1.0f) |
+                   !(m.z >= 0.0f && m.z <= 1.0f) | !(m.w >= 0.0f && m.w <= 1.0f);
+            reinterpret_cast<float4*>(dist)[i] = make_float4(
+                init_value(m.x, nu), init_value(m.y, nu), init_value(m.z, nu), init_value(m.w, nu));
+            if (img) {
+                const float4 a = reinterpret_cast<const float4*>(img)[i];
+                st.add(a.x); st.add(a.y); st.add(a.z); st.add(a.w);
+            }
+        }
+    } else {
+        for (long long i = t0; i < n; i += stride) {
+            const long long om = vox_offset(mv, i);
+            const float m = mask[om];
+            bad |= !(m >= 0.0f && m <= 1.0f);
+            dist[vox_offset(dv, i)] = init_value(m, nu);
+            if (img) st.add(img[om]);
+        }
+    }
+    flush_check(st, bad, out);
+}
+
+// Exactness / mask-range check alone (scans that are not generalized_geodesic).
+__global__ void image_check_kernel(VolView v, const float* img, const float* mask,
+                                   ImageCheck* out, long long n) {
+    ExpStats st;
+    int bad = 0;
+    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    const long long t0 = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (dense(v) && (n & 3) == 0) {
+        const long long n4 = n >> 2;
+        for (long long i = t0; i < n4; i += stride) {
+            if (img) {
+                const float4 a = reinterpret_cast<const float4*>(img)[i];
+                st.add(a.x); st.add(a.y); st.add(a.z); st.add(a.w);
+            }
+            if (mask) {
+                const float4 m = reinterpret_cast<const float4*>(mask)[i];
+                bad |= !(m.x >= 0.0f && m.x <= 1.0f) | !(m.y >= 0.0f && m.y <= 1.0f) |
+                       !(m.z >= 0.0f && m.z <= 1.0f) | !(m.w >= 0.0f && m.w <= 1.0f);
+            }
+        }
+    } else {
+        for (long long i = t0; i < n; i += stride) {
+            const long long o = vox_offset(v, i);
+            if (img) st.add(img[o]);
+            if (mask) {
+                const float m = mask[o];
+                bad |= !(m >= 0.0f && m <= 1.0f);
+            }
+        }
+    }
+    flush_check(st, bad, out);
+}
+
+// 64x64-tile transpose of every (b, z) slice between the canonical layout
+// [b][z][y][x] (row pitch c.ys, slice pitch c.zs) and the x-sweep layout
+// [b][x][z][y] (x pitch t.zs, z pitch t.ys).  FWD: canonical -> x-layout.
+// Loads and stores are float4 along the contiguous axis of each side; the
+// 64x65 shared tile keeps the column reads to 2-way bank conflicts.
+template <bool FWD>
+__global__ void __launch_bounds__(256) transpose_kernel(VolView cv, VolView tv, const float* src,
+                                                        float* dst, int tiles_a, int tiles_b,
+                                                        long long ntiles) {
+    __shared__ float tile[64][65];
+    const int D = cv.D, H = cv.H, W = cv.W;
+    // FWD: tile rows = y (input rows), cols = x.  BWD: tile rows = x, cols = y.
+    const int RA = FWD ? H : W;   // extent of the input row axis
+    const int CA = FWD ? W : H;   // extent of the input contiguous axis
+    const int tid = threadIdx.x;
+    const int lr = tid >> 4;          // 0..15
+    const int lc = (tid & 15) * 4;    // 0..60
+    for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int ta = static_cast<int>(t % tiles_a);
+        const long long rest = t / tiles_a;
+        const int tb = static_cast<int>(rest % tiles_b);
+        const long long bz = rest / tiles_b;
+        const int z = static_cast<int>(bz % D);
+        const long long b = bz / D;
+        const int r0 = tb * 64, c0 = ta * 64;
+        const float* sbase;
+        long long s_row;
+        if (FWD) {
+            sbase = src + b * cv.vol + z * cv.zs;
+            s_row = cv.ys;
+        } else {
+            sbase = src + b * tv.vol + z * tv.ys;
+            s_row = tv.zs;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int r = r0 + i * 16 + lr, cc = c0 + lc;
+            float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f;
+            if (r < RA) {
+                const float* q = sbase + r * s_row + cc;
+                if (cc + 3 < CA) {
+                    const float4 a = *reinterpret_cast<const float4*>(q);
+                    v0 = a.x; v1 = a.y; v2 = a.z; v3 = a.w;
+                } else {
+                    if (cc < CA) v0 = q[0];
+                    if (cc + 1 < CA) v1 = q[1];
+                    if (cc + 2 < CA) v2 = q[2];
+                }
+            }
+            float* trow = tile[i * 16 + lr];
+            trow[lc] = v0; trow[lc + 1] = v1; trow[lc + 2] = v2; trow[lc + 3] = v3;
+        }
+        __syncthreads();
+        float* dbase;
+        long long d_row;
+        if (FWD) {
+            dbase = dst + b * tv.vol + z * tv.ys;
+            d_row = tv.zs;
+        } else {
+            dbase = dst + b * cv.vol + z * cv.zs;
+            d_row = cv.ys;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int oc = i * 16 + lr;     // output row = input column
+            const int orow = c0 + oc;
+            const int ocol = r0 + lc;       // output contiguous = input row axis
+            if (orow < CA) {
+                const float v0 = tile[lc][oc], v1 = tile[lc + 1][oc], v2 = tile[lc + 2][oc],
+                            v3 = tile[lc + 3][oc];
+                float* q = dbase + orow * d_row + ocol;
+                if (ocol + 3 < RA) {
+                    *reinterpret_cast<float4*>(q) = make_float4(v0, v1, v2, v3);
+                } else {
+                    if (ocol < RA) q[0] = v0;
+                    if (ocol + 1 < RA) q[1] = v1;
+                    if (ocol + 2 < RA) q[2] = v2;
+                }
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -144,9 +238,8 @@ __global__ void gsf_sources_kernel(VolView v, const float* mask, VolView o, floa
                                    long long n) {
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        int ok;
-        const float m = mask[vox_offset(v, i, ok)];
-        out[vox_offset(o, i, ok)] = m >= 0.5f ? 0.0f : 1.0f;
+        const float m = mask[vox_offset(v, i)];
+        out[vox_offset(o, i)] = m >= 0.5f ? 0.0f : 1.0f;
     }
 }
 
@@ -157,8 +250,7 @@ __global__ void gsf_dilate_kernel(VolView v, const float* dist, float* out, doub
     unsigned long long cnt = 0;
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        int ok;
-        const long long o = vox_offset(v, i, ok);
+        const long long o = vox_offset(v, i);
         const float dil = static_cast<double>(dist[o]) <= theta ? 1.0f : 0.0f;
         out[o] = dil;
         cnt += dil >= 0.5f ? 0 : 1;
@@ -172,22 +264,20 @@ __global__ void gsf_erode_kernel(VolView v, const float* dist, VolView o, float*
                                  long long n) {
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        int ok;
-        const float d = dist[vox_offset(v, i, ok)];
-        out[vox_offset(o, i, ok)] = static_cast<double>(d) > theta ? 1.0f : 0.0f;
+        const float d = dist[vox_offset(v, i)];
+        out[vox_offset(o, i)] = static_cast<double>(d) > theta ? 1.0f : 0.0f;
     }
 }
 
 // Fixpoint change: max over voxels of f64(before) - f64(after) (scan_parallel.cpp:386-392).
-// Non-negative values only matter (change starts at 0), so the f64 bit pattern
+// Only non-negative values matter (change starts at 0), so the f64 bit pattern
 // orders like an unsigned integer.
 __global__ void max_change_kernel(VolView v, const float* before, const float* after,
                                   unsigned long long* out, long long n) {
     double m = 0.0;
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        int ok;
-        const long long o = vox_offset(v, i, ok);
+        const long long o = vox_offset(v, i);
         const double c = static_cast<double>(before[o]) - static_cast<double>(after[o]);
         m = c > m ? c : m;
     }
@@ -209,7 +299,7 @@ __global__ void splitmix_kernel(float* out, long long n, unsigned long long seed
     }
 }
 
-int grid_for(long long n, int threads) {
+int sm_count() {
     static int sms = 0;
     if (!sms) {
         int dev = 0;
@@ -217,35 +307,51 @@ int grid_for(long long n, int threads) {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         if (sms <= 0) sms = 148;
     }
+    return sms;
+}
+
+int grid_for(long long n, int threads) {
     const long long need = (n + threads - 1) / threads;
-    const long long cap = static_cast<long long>(sms) * 8;
+    const long long cap = static_cast<long long>(sm_count()) * 8;
     return static_cast<int>(need < cap ? (need > 0 ? need : 1) : cap);
 }
 
 }  // namespace
 
 cudaError_t launch_init_generalized(const VolView& m, const VolView& d, const float* mask,
-                                    float* dist, double nu, cudaStream_t s) {
+                                    float* dist, double nu, ImageCheck* check, const float* img,
+                                    cudaStream_t s) {
     const long long n = m.count();
-    init_generalized_kernel<<<grid_for(n, 256), 256, 0, s>>>(m, d, mask, dist, nu, n);
+    if (check) {
+        ImageCheck init{-1000, 1000, 0, 0, 0, 0};
+        cudaError_t e = cudaMemcpyAsync(check, &init, sizeof(init), cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) return e;
+    }
+    // a scratch check target when the caller does not want one
+    static ImageCheck* dummy = nullptr;
+    if (!check) {
+        if (!dummy && cudaMalloc(&dummy, sizeof(ImageCheck)) != cudaSuccess) return cudaErrorMemoryAllocation;
+        check = dummy;
+        img = nullptr;
+    }
+    init_check_kernel<<<grid_for((n + 3) / 4, 256), 256, 0, s>>>(m, d, img, mask, dist, nu, check, n);
     return cudaGetLastError();
 }
 
 cudaError_t launch_transpose(const VolView& src_v, const VolView& dst_v, const float* src,
                              float* dst, bool forward, cudaStream_t s) {
-    // src_v / dst_v carry the logical (D, H, W) of the [z][y][x] volume in both
-    // directions; zs/ys/vol are the respective layouts' strides.
-    const VolView& lv = forward ? src_v : dst_v;
-    dim3 grid((lv.W + 31) / 32, (lv.H + 31) / 32, std::min(lv.D * lv.B, 65535));
-    dim3 block(32, 8);
-    VolView a = src_v, b = dst_v;
-    a.D = b.D = lv.D;
-    a.H = b.H = lv.H;
-    a.W = b.W = lv.W;
+    // forward: src canonical -> dst x-layout; backward: src x-layout -> dst canonical.
+    const VolView& cv = forward ? src_v : dst_v;
+    const VolView& tv = forward ? dst_v : src_v;
+    const int RA = forward ? cv.H : cv.W, CA = forward ? cv.W : cv.H;
+    const int tiles_a = (CA + 63) / 64, tiles_b = (RA + 63) / 64;
+    const long long ntiles = static_cast<long long>(tiles_a) * tiles_b * cv.D * cv.B;
+    const long long cap = static_cast<long long>(sm_count()) * 8;
+    const int grid = static_cast<int>(ntiles < cap ? ntiles : cap);
     if (forward)
-        transpose_kernel<true><<<grid, block, 0, s>>>(a, b, src, dst);
+        transpose_kernel<true><<<grid, 256, 0, s>>>(cv, tv, src, dst, tiles_a, tiles_b, ntiles);
     else
-        transpose_kernel<false><<<grid, block, 0, s>>>(a, b, src, dst);
+        transpose_kernel<false><<<grid, 256, 0, s>>>(cv, tv, src, dst, tiles_a, tiles_b, ntiles);
     return cudaGetLastError();
 }
 
@@ -255,7 +361,7 @@ cudaError_t launch_image_check(const VolView& v, const float* img, const float* 
     ImageCheck init{-1000, 1000, 0, 0, 0, 0};
     cudaError_t e = cudaMemcpyAsync(out, &init, sizeof(init), cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return e;
-    image_check_kernel<<<grid_for(n, 256), 256, 0, s>>>(v, img, mask, out, n);
+    image_check_kernel<<<grid_for((n + 3) / 4, 256), 256, 0, s>>>(v, img, mask, out, n);
     return cudaGetLastError();
 }
 

@@ -20,8 +20,11 @@ struct ImageCheck {
     int emax, tmin, pos, neg, bad_mask, nonfinite;
 };
 
+// Soft-mask init (transforms.cpp:150-156) fused with the mask-range and
+// image-exactness reduction into `check` (reset here); `img`/`check` may be null.
 cudaError_t launch_init_generalized(const VolView& m, const VolView& d, const float* mask,
-                                    float* dist, double nu, cudaStream_t s);
+                                    float* dist, double nu, ImageCheck* check, const float* img,
+                                    cudaStream_t s);
 cudaError_t launch_transpose(const VolView& src_v, const VolView& dst_v, const float* src,
                              float* dst, bool forward, cudaStream_t s);
 cudaError_t launch_image_check(const VolView& v, const float* img, const float* mask,

@@ -202,16 +202,8 @@ struct Prepared {
     bool mask_ok = true;
 };
 
-Status check_inputs(StreamCtx& sc, const Work& w, const float* mask, bool want_img,
-                    cudaStream_t s, Prepared* out) {
-    GD_ST(sc.small.ensure(256));
-    ImageCheck* dev = sc.small.as<ImageCheck>();
-    VolView v = w.canon();
-    {
-        ProfScope ps(kProfOther, 4.0 * w.B * w.g.voxels() * ((want_img ? 1 : 0) + (mask ? 1 : 0)), s);
-        GD_CK(launch_image_check(v, want_img ? w.img : nullptr, mask, dev, s));
-    }
-    ++g_launches;
+// Reads back an ImageCheck (synchronising the stream) and interprets it.
+Status read_check(const ImageCheck* dev, cudaStream_t s, Prepared* out) {
     ImageCheck h;
     GD_CK(cudaMemcpyAsync(&h, dev, sizeof(h), cudaMemcpyDeviceToHost, s));
     GD_CK(cudaStreamSynchronize(s));
@@ -225,6 +217,19 @@ Status check_inputs(StreamCtx& sc, const Work& w, const float* mask, bool want_i
         out->exact_diff = (h.emax - h.tmin) <= limit;
     }
     return Status::Ok();
+}
+
+Status check_inputs(StreamCtx& sc, const Work& w, const float* mask, bool want_img,
+                    cudaStream_t s, Prepared* out) {
+    GD_ST(sc.small.ensure(256));
+    ImageCheck* dev = sc.small.as<ImageCheck>();
+    VolView v = w.canon();
+    {
+        ProfScope ps(kProfOther, 4.0 * w.B * w.g.voxels() * ((want_img ? 1 : 0) + (mask ? 1 : 0)), s);
+        GD_CK(launch_image_check(v, want_img ? w.img : nullptr, mask, dev, s));
+    }
+    ++g_launches;
+    return read_check(dev, s, out);
 }
 
 Status ensure_x_layout(StreamCtx& sc, Work& w, bool need_img, cudaStream_t s) {
@@ -497,25 +502,23 @@ Status generalized_locked(StreamCtx& sc, const GridDesc& g, int B, const float* 
     GD_ST(bind(sc, w, g, B, img, out, false, s, &padded));
     const int kind = cost_kind(lambda);
     Prepared prep;
-    // mask range is checked on the caller's (dense) mask; image on the working copy.
-    {
-        Work wm = w;
-        wm.Wp = g.W;
-        wm.zs = static_cast<long long>(g.H) * g.W;
-        wm.vol = static_cast<long long>(g.D) * wm.zs;
-        wm.img = img;
-        GD_ST(check_inputs(sc, wm, mask, kind == kIntensity, s, &prep));
-    }
-    if (!prep.mask_ok)
-        return Status::Invalid("generalized_geodesic: mask values must lie in [0, 1]");
+    // One pass over the caller's (dense) image + mask: soft-mask init into the
+    // working distance, mask-range check, image-exactness statistics.
     VolView mv;
     mv.B = B; mv.D = g.D; mv.H = g.H; mv.W = g.W;
     mv.zs = static_cast<long long>(g.H) * g.W; mv.ys = g.W; mv.vol = g.D * mv.zs;
+    GD_ST(sc.small.ensure(256));
+    ImageCheck* chk = sc.small.as<ImageCheck>();
+    const bool want_img = kind == kIntensity;
     {
-        ProfScope ps(kProfInit, 8.0 * B * g.voxels(), s);
-        GD_CK(launch_init_generalized(mv, w.canon(), mask, w.dist, nu, s));
+        ProfScope ps(kProfInit, (want_img ? 12.0 : 8.0) * B * g.voxels(), s);
+        GD_CK(launch_init_generalized(mv, w.canon(), mask, w.dist, nu, chk,
+                                      want_img ? img : nullptr, s));
     }
     ++g_launches;
+    GD_ST(read_check(chk, s, &prep));
+    if (!prep.mask_ok)
+        return Status::Invalid("generalized_geodesic: mask values must lie in [0, 1]");
     GD_ST(scan_work(sc, w, lambda, iterations, pick_f64(kind, prep), s, st));
     if (padded) GD_ST(unbind(w, out, s));
     return Status::Ok();
