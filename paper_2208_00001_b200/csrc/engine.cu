@@ -368,6 +368,8 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
             GD_ST(sc.trace.ensure(trace_n * sizeof(long long)));
             GD_CK(cudaMemsetAsync(sc.trace.p, 0, trace_n * sizeof(long long), s));
             p.trace = sc.trace.as<long long>();
+            static const int dbg = std::getenv("GEODIST_SWEEP_DEBUG") ? std::atoi(std::getenv("GEODIST_SWEEP_DEBUG")) : 0;
+            p.debug_flags = dbg;
         }
         {
             const double bytes = static_cast<double>(nvol) * g.voxels() * npass *
@@ -382,21 +384,22 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
             GD_CK(cudaStreamSynchronize(s));
             const int nw = nwv * (R == 1 ? 1 : (R == 2 ? 1 : 2));
             for (int w = 0; w < nw; ++w) {
-                double acc[6] = {0, 0, 0, 0, 0, 0};
+                double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
                 long long n = 0;
                 for (long long cta = 0; cta < nvol * per_vol; ++cta) {
                     const long long* o = &h[(cta * 64 + w) * 8];
                     if (o[5] == 0) continue;
-                    for (int k = 0; k < 6; ++k) acc[k] += o[k];
+                    for (int k = 0; k < 8; ++k) acc[k] += o[k];
                     ++n;
                 }
                 if (!n) continue;
                 const double steps = acc[5] / n;
                 std::fprintf(stderr,
                              "trace axis=%d warp=%d: cycles/step total %.0f tma %.0f spin %.0f "
-                             "barrier %.0f reloads/step %.2f (ctas %lld)\n",
+                             "barrier %.0f reloads/step %.2f phaseA %.0f tail %.0f (ctas %lld)\n",
                              axis, w, acc[4] / n / steps, acc[0] / n / steps, acc[1] / n / steps,
-                             acc[2] / n / steps, acc[3] / n / steps, n);
+                             acc[2] / n / steps, acc[3] / n / steps, acc[6] / n / steps,
+                             acc[7] / n / steps, n);
             }
         }
         ++g_launches;

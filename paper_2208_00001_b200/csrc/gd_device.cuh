@@ -58,15 +58,23 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 }
 
 // ---- tagged halo words: {f32 value, u32 tag} in one single-copy-atomic b64 --
+// Memory-model qualifiers of the halo accesses (relaxed, GPU scope: coherent at
+// L2, 8-byte single-copy atomic).  Overridable for experiments.
+#ifndef GD_HALO_LD
+#define GD_HALO_LD "ld.relaxed.gpu.global"
+#endif
+#ifndef GD_HALO_ST
+#define GD_HALO_ST "st.relaxed.gpu.global"
+#endif
 __device__ __forceinline__ void st_tagged(unsigned long long* p, float v, uint32_t tag) {
     const unsigned long long w =
         (static_cast<unsigned long long>(tag) << 32) | __float_as_uint(v);
-    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
+    asm volatile("" GD_HALO_ST ".b64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
 }
 
 __device__ __forceinline__ unsigned long long ld_tagged(const unsigned long long* p) {
     unsigned long long w;
-    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+    asm volatile("" GD_HALO_LD ".b64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
     return w;
 }
 
@@ -75,13 +83,13 @@ __device__ __forceinline__ unsigned long long ld_tagged(const unsigned long long
 __device__ __forceinline__ void st_tagged2(unsigned long long* p, float v0, float v1, uint32_t tag) {
     const unsigned long long w0 = (static_cast<unsigned long long>(tag) << 32) | __float_as_uint(v0);
     const unsigned long long w1 = (static_cast<unsigned long long>(tag) << 32) | __float_as_uint(v1);
-    asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(w0), "l"(w1)
+    asm volatile("" GD_HALO_ST ".v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(w0), "l"(w1)
                  : "memory");
 }
 
 __device__ __forceinline__ void ld_tagged2(const unsigned long long* p, unsigned long long& w0,
                                            unsigned long long& w1) {
-    asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(p)
+    asm volatile("" GD_HALO_LD ".v2.b64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(p)
                  : "memory");
 }
 

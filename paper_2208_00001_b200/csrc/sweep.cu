@@ -111,9 +111,11 @@ constexpr bool kDualPoll = false;
 #ifdef GD_SWEEP_TRACE
 #define GD_T0(v) const long long v = clock64()
 #define GD_TADD(slot, v) trc[slot] += clock64() - (v)
+#define GD_DBG(bit) ((p.debug_flags & (bit)) != 0)
 #else
 #define GD_T0(v)
 #define GD_TADD(slot, v)
+#define GD_DBG(bit) false
 #endif
 
 // The 3-column windows of one previous-plane row for a lane's 4 columns:
@@ -281,6 +283,7 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
         const int par = j & 1;
         const uint32_t tag = tag_base + static_cast<uint32_t>(j);
         unsigned long long* q = self0 + par * 2ll * VW;
+        if (GD_DBG(2)) return;
         if (pub_up) {
             st_tagged2(q, N[0][0], N[0][1], tag);
             st_tagged2(q + 2, N[0][2], N[0][3], tag);
@@ -311,7 +314,7 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
 
     float PA[RW][kC], IA[RW][kC], PB[RW][kC], IB[RW][kC];
 #ifdef GD_SWEEP_TRACE
-    long long trc[6] = {0, 0, 0, 0, 0, 0};  // tma wait, halo spin, barrier, reloads, total, steps
+    long long trc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // tma, spin, barrier, reloads, total, steps, phaseA, tail
     const long long t_begin = clock64();
 #endif
 
@@ -377,12 +380,15 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
             ld_tagged2(q + 2, h[3], h[4]);
             h[5] = ld_tagged(q + dr);
         };
-        if (TOP && has_up) load_row(hup, huA);
-        if (BOT && has_dn) load_row(hdn, hdA);
+        if (!GD_DBG(4)) {
+            if (TOP && has_up) load_row(hup, huA);
+            if (BOT && has_dn) load_row(hdn, hdA);
+        }
 
         GD_T0(t_tma);
         mbar_wait(&c.full[slot], phase);
         GD_TADD(0, t_tma);
+        GD_T0(t_pa);
         float dold[RW][kC], ic[RW][kC];
 #pragma unroll
         for (int r = 0; r < RW; ++r) {
@@ -461,6 +467,9 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
         }
 
         // ---- phase B: rows above / below the strip (tagged halo) -------------
+#ifdef GD_SWEEP_TRACE
+        long long t_tail0_outer = 0;
+#endif
         if (TOP || BOT) {
             auto fresh = [&](const unsigned long long (&h)[6]) {
                 bool ok = true;
@@ -469,9 +478,10 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
                 return ok;
             };
             long long spins = 0;
+            GD_TADD(6, t_pa);
             GD_T0(t_spin);
             bool useB = false;
-            while (true) {
+            while (!GD_DBG(1)) {
                 const bool ok = useB ? ((!(TOP && has_up) || fresh(huB)) &&
                                         (!(BOT && has_dn) || fresh(hdB)))
                                      : ((!(TOP && has_up) || fresh(huA)) &&
@@ -488,6 +498,9 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
                 if (++spins > kSpinLimit) __trap();
             }
             GD_TADD(1, t_spin);
+#ifdef GD_SWEEP_TRACE
+            t_tail0_outer = clock64();
+#endif
 #ifdef GD_SWEEP_TRACE
             trc[3] += spins;
 #endif
@@ -565,6 +578,9 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
         if (near_turn) fence_proxy_async_global();
 
         GD_T0(t_bar);
+#ifdef GD_SWEEP_TRACE
+        if (TOP || BOT) trc[7] += t_bar - t_tail0_outer;
+#endif
         consumer_sync(nthreads);
         GD_TADD(2, t_bar);
         if (tid == 0 && near_turn) st_release_cta(c.progress, j);
@@ -581,7 +597,7 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
     trc[5] = J;
     if (p.trace && lane == 0) {
         long long* o = p.trace + (static_cast<long long>(c.g) * 64 + wu * nwv + wv) * 8;
-        for (int i = 0; i < 6; ++i) o[i] = trc[i];
+        for (int i = 0; i < 8; ++i) o[i] = trc[i];
     }
 #endif
 }

@@ -74,6 +74,7 @@ struct SweepParams {
     uint32_t tag_base;
     unsigned long long* halo; // tagged halo words: [strip][parity][TOP|BOT][nwv*128]
     long long* trace;         // optional per-warp cycle counters (null in production)
+    int debug_flags;          // experiments only (GD_SWEEP_TRACE builds): 1 no spin, 2 no halo stores, 4 no halo loads
     // Neighbour coefficients indexed (du+1)*3 + (dv+1).
     double rho[9];
     double c0[9];
