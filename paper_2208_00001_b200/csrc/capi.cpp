@@ -11,6 +11,10 @@
 #include "../../include/geodist_b200.h"
 #include "engine.cuh"
 
+namespace gdb {
+int sweep_max_coresident(int R, int nwv, int kind, bool f64);  // sweep.cu
+}
+
 namespace {
 
 thread_local std::string t_err;
@@ -227,3 +231,8 @@ int gd_fill_splitmix(float* device_out, long long n, unsigned long long seed, vo
 }
 
 }  // extern "C"
+
+// Diagnostics: co-resident CTA capacity of one sweep configuration.
+extern "C" int gd_debug_coresident(int R, int nwv, int kind, int f64) {
+    return gdb::sweep_max_coresident(R, nwv, kind, f64 != 0);
+}

@@ -287,7 +287,14 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
     // R = 4 (enough rows to hide the halo latency behind the strip interior).
     int R = 0, maxc = 0;
     long long per_vol = 0;
-    const int pref[] = {4, 8, 2, 1};
+    int pref[] = {4, 8, 2, 1};
+    // Tuning override (experiments): GEODIST_SWEEP_R=<rows per strip> tried first.
+    static const int r_env = std::getenv("GEODIST_SWEEP_R") ? std::atoi(std::getenv("GEODIST_SWEEP_R")) : 0;
+    if (r_env == 1 || r_env == 2 || r_env == 8) {
+        for (int& x : pref)
+            if (x == r_env) x = 4;
+        pref[0] = r_env;
+    }
     for (int cand : pref) {
         if (nu == 1 && cand != 1) continue;
         if (nwv > 4 && cand == 8) continue;
@@ -395,9 +402,9 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
                 if (!n) continue;
                 const double steps = acc[5] / n;
                 std::fprintf(stderr,
-                             "trace axis=%d warp=%d: cycles/step total %.0f tma %.0f spin %.0f "
+                             "trace axis=%d R=%d maxc=%d warp=%d: cycles/step total %.0f tma %.0f spin %.0f "
                              "barrier %.0f reloads/step %.2f phaseA %.0f tail %.0f (ctas %lld)\n",
-                             axis, w, acc[4] / n / steps, acc[0] / n / steps, acc[1] / n / steps,
+                             axis, R, maxc, w, acc[4] / n / steps, acc[0] / n / steps, acc[1] / n / steps,
                              acc[2] / n / steps, acc[3] / n / steps, acc[6] / n / steps,
                              acc[7] / n / steps, n);
             }

@@ -607,6 +607,9 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
 // released ("empty") by every consumer warp during step j+1, which reads it as
 // the previous plane's intensities.
 template <int KIND, bool F64, int RW, int NWU, int NST, int MW>
+// One CTA per SM: two R = 2 CTAs per SM (126-register cap) measured 1.66 vs
+// 1.25 us/step for R = 4 at 512^3 -- twice the halo links cost more than the
+// second CTA hides (profiles/README.md).
 __global__ void __launch_bounds__((MW * NWU + 1) * 32, 1)
     sweep_kernel(const __grid_constant__ CUtensorMap tm_d, const __grid_constant__ CUtensorMap tm_i,
                  const __grid_constant__ SweepParams p) {
