@@ -165,15 +165,6 @@ struct Layout {
     }
 };
 
-// Relaxed loads of one halo row's window: words v-1 .. v+4 of the published row.
-__device__ __forceinline__ void load_halo_row(const unsigned long long* q, bool has_left,
-                                              bool has_right, unsigned long long (&h)[6]) {
-    h[0] = has_left ? ld_tagged(q - 1) : 0ull;
-    ld_tagged2(q, h[1], h[2]);
-    ld_tagged2(q + 2, h[3], h[4]);
-    h[5] = has_right ? ld_tagged(q + 4) : 0ull;
-}
-
 // A previous-plane row window for this lane: own 4 columns from `c4`, the
 // neighbours v-1 / v+4 from the adjacent lanes, and at the warp edges from
 // `edge_l` / `edge_r` (column 128wv-1 / 128wv+128).
@@ -185,6 +176,21 @@ __device__ __forceinline__ void make_window(const float (&c4)[kC], float edge_l,
     const float dn = __shfl_down_sync(kFull, c4[0], 1);
     win[0] = lane == 0 ? edge_l : up;
     win[5] = lane == 31 ? edge_r : dn;
+}
+
+// Window of a fresh halo row: own words h[1..4], neighbour lanes' edge words by
+// shuffle, h[0] / h[5] at the warp edges; INF outside the plane or strip set.
+__device__ __forceinline__ void halo_window(const unsigned long long (&h)[6], bool present,
+                                            bool has_left, bool has_right, int lane,
+                                            float (&win)[6]) {
+    const float inf = __int_as_float(0x7f800000);
+    const float c4[kC] = {val_of(h[1]), val_of(h[2]), val_of(h[3]), val_of(h[4])};
+    make_window(c4, val_of(h[0]), val_of(h[5]), lane, win);
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+        if (!present) win[i] = inf;
+    if (!has_left) win[0] = inf;
+    if (!has_right) win[5] = inf;
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -245,13 +251,17 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
     const bool has_up = TOP && c.tu > 0, has_dn = BOT && c.tu + 1 < p.ntu;
     const long long strip_words = 2ll * 2 * VW;  // per strip: 2 parities x {TOP, BOT}
     const long long strip0 = static_cast<long long>(c.b) * p.ntu;
-    // Halo row windows, one pointer per parity.  Lanes at the plane's edge
-    // point their v-1 / v+4 word at their own first word (value unused).
+    // Halo row layout (per warp column block of 128 words): columns q = 0,1 of
+    // all 32 lanes, then q = 2,3 -- lane l owns words 2l, 2l+1, 64+2l, 65+2l, so
+    // each 16-byte access of the warp covers 512 contiguous bytes (16 full
+    // sectors) instead of half of 32 sectors.  v-1 / v+4 come from the adjacent
+    // lanes; only lane 0 / lane 31 load the neighbour block's edge word.
     const bool has_left = vl > 0, has_right = vl + kC < p.nv;
-    const int dl = has_left ? -1 : 0, dr = has_right ? kC : 0;
-    const unsigned long long* up0 = p.halo + (strip0 + c.tu - 1) * strip_words + VW + vl;
-    const unsigned long long* dn0 = p.halo + (strip0 + c.tu + 1) * strip_words + vl;
-    unsigned long long* self0 = p.halo + static_cast<long long>(c.g) * strip_words + vl;
+    const bool edge_l = lane == 0 && has_left, edge_r = lane == 31 && has_right;
+    const int hl = wv * kWV + 2 * lane;
+    const unsigned long long* up0 = p.halo + (strip0 + c.tu - 1) * strip_words + VW + hl;
+    const unsigned long long* dn0 = p.halo + (strip0 + c.tu + 1) * strip_words + hl;
+    unsigned long long* self0 = p.halo + static_cast<long long>(c.g) * strip_words + hl;
     const bool pub_up = TOP && c.tu > 0, pub_dn = BOT && c.tu + 1 < p.ntu;
     // neighbour-warp edge columns
     const int eoffL = ((wu * nwv + wv - 1) * 2 + 1) * RW;
@@ -286,11 +296,11 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
         if (GD_DBG(2)) return;
         if (pub_up) {
             st_tagged2(q, N[0][0], N[0][1], tag);
-            st_tagged2(q + 2, N[0][2], N[0][3], tag);
+            st_tagged2(q + 64, N[0][2], N[0][3], tag);
         }
         if (pub_dn) {
             st_tagged2(q + VW, N[RW - 1][0], N[RW - 1][1], tag);
-            st_tagged2(q + VW + 2, N[RW - 1][2], N[RW - 1][3], tag);
+            st_tagged2(q + VW + 64, N[RW - 1][2], N[RW - 1][3], tag);
         }
     };
     auto publish_smem = [&](int j, const float (&N)[RW][kC]) {
@@ -375,10 +385,10 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
         // between them so a fresh word is seen within about half a round trip.
         unsigned long long huA[6], hdA[6], huB[6], hdB[6];  // [0] = v-1, [1..4] own, [5] = v+4
         auto load_row = [&](const unsigned long long* q, unsigned long long (&h)[6]) {
-            h[0] = ld_tagged(q + dl);
             ld_tagged2(q, h[1], h[2]);
-            ld_tagged2(q + 2, h[3], h[4]);
-            h[5] = ld_tagged(q + dr);
+            ld_tagged2(q + 64, h[3], h[4]);
+            h[0] = edge_l ? ld_tagged(q - 1) : 0ull;   // previous block, last word
+            h[5] = edge_r ? ld_tagged(q + 66) : 0ull;  // next block, first word
         };
         if (!GD_DBG(4)) {
             if (TOP && has_up) load_row(hup, huA);
@@ -472,9 +482,9 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
 #endif
         if (TOP || BOT) {
             auto fresh = [&](const unsigned long long (&h)[6]) {
-                bool ok = true;
+                bool ok = (!edge_l || tag_of(h[0]) == want) && (!edge_r || tag_of(h[5]) == want);
 #pragma unroll
-                for (int i = 0; i < 6; ++i) ok = ok && tag_of(h[i]) == want;
+                for (int i = 1; i <= kC; ++i) ok = ok && tag_of(h[i]) == want;
                 return ok;
             };
             long long spins = 0;
@@ -512,19 +522,13 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
             }
             if (TOP) {
                 float pw[6], iw[6];
-#pragma unroll
-                for (int i = 0; i < 6; ++i) pw[i] = has_up ? val_of(hu[i]) : INF;
-                if (!has_left) pw[0] = INF;
-                if (!has_right) pw[5] = INF;
+                halo_window(hu, has_up, has_left, has_right, lane, pw);
                 i_window(-1, iw);
                 relax_row<KIND, F64>(acc[0], pw, iw, ic[0], -1, p);
             }
             if (BOT) {
                 float pw[6], iw[6];
-#pragma unroll
-                for (int i = 0; i < 6; ++i) pw[i] = has_dn ? val_of(hd[i]) : INF;
-                if (!has_left) pw[0] = INF;
-                if (!has_right) pw[5] = INF;
+                halo_window(hd, has_dn, has_left, has_right, lane, pw);
                 i_window(R, iw);
                 relax_row<KIND, F64>(acc[RW - 1], pw, iw, ic[RW - 1], +1, p);
             }
