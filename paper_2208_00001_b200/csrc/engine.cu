@@ -283,28 +283,32 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
     if (nwv > kMaxWarps)
         return {kUnsupported, "plane width " + std::to_string(nv) + " exceeds " +
                                   std::to_string(kMaxWarps * kWV) + " columns"};
-    // Rows per strip: the smallest R whose strips are all co-resident, preferring
-    // R = 4 (enough rows to hide the halo latency behind the strip interior).
+    // Rows per strip.  Every strip of a volume must be co-resident (the halo
+    // chain spins); volumes beyond what fits run in sequential launch groups.
+    // Cost = groups x relative per-step cost of the strip shape (taller strips
+    // do more work per step; measured on B200).  A single large volume keeps
+    // R = 4 (enough rows to cover the halo latency, strips on every SM);
+    // batches of small volumes take taller strips so fewer groups run.
     int R = 0, maxc = 0;
     long long per_vol = 0;
-    int pref[] = {4, 8, 2, 1};
-    // Tuning override (experiments): GEODIST_SWEEP_R=<rows per strip> tried first.
-    static const int r_env = std::getenv("GEODIST_SWEEP_R") ? std::atoi(std::getenv("GEODIST_SWEEP_R")) : 0;
-    if (r_env == 1 || r_env == 2 || r_env == 8) {
-        for (int& x : pref)
-            if (x == r_env) x = 4;
-        pref[0] = r_env;
-    }
-    for (int cand : pref) {
-        if (nu == 1 && cand != 1) continue;
-        if (nwv > 4 && cand == 8) continue;
+    static const int r_env =
+        std::getenv("GEODIST_SWEEP_R") ? std::atoi(std::getenv("GEODIST_SWEEP_R")) : 0;
+    double best = 0.0;
+    for (int cand : {4, 8, 16, 2, 1}) {
+        if ((nu == 1) != (cand == 1)) continue;
+        if (sweep_warp_rows(cand, nwv) == 0) continue;
         const int mc = sweep_max_coresident(cand, nwv, kind, f64);
         const long long pv = (nu + cand - 1) / cand;
-        if (mc > 0 && pv <= mc) {
+        if (mc <= 0 || pv > mc) continue;
+        const long long groups = (w.B + mc / pv - 1) / (mc / pv);
+        const double rel = cand <= 4 ? 1.0 : (cand == 8 ? 1.4 : 2.0);
+        double cost = static_cast<double>(groups) * rel;
+        if (cand == r_env) cost = -1.0;  // tuning override (experiments)
+        if (R == 0 || cost < best) {
             R = cand;
             maxc = mc;
             per_vol = pv;
-            break;
+            best = cost;
         }
     }
     if (R == 0)
@@ -389,7 +393,7 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
             GD_CK(cudaMemcpyAsync(h.data(), sc.trace.p, trace_n * sizeof(long long),
                                   cudaMemcpyDeviceToHost, s));
             GD_CK(cudaStreamSynchronize(s));
-            const int nw = nwv * (R == 1 ? 1 : (R == 2 ? 1 : 2));
+            const int nw = nwv * sweep_warp_rows(R, nwv);
             for (int w = 0; w < nw; ++w) {
                 double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
                 long long n = 0;

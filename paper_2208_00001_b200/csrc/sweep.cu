@@ -34,6 +34,12 @@ __device__ __forceinline__ float2 f2_add(float2 a, float2 b) {
     return bits_f2(r);
 }
 
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float r;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 // One relaxation candidate d_q + cost(p, q) rounded to f32 (see sweep.cuh for
 // why per-candidate rounding is exact).  k = (du+1)*3 + (dv+1).
 template <int KIND, bool F64>
@@ -55,8 +61,10 @@ __device__ __forceinline__ float candidate(float pq, float iq, float ip, int k,
             return static_cast<float>(static_cast<double>(pq) +
                                       sqrt(fma(p.lambda * di, di, p.c0[k])));
         } else {
+            // MUFU.SQRT (about 1 ulp): the IEEE sqrtf adds a slow-path CALL per
+            // candidate that serialises the 9-candidate min (3x slower step).
             const float di = ip - iq;
-            return pq + sqrtf(fmaf(p.lambda_f * di, di, p.c0_f[k]));
+            return pq + sqrt_approx(fmaf(p.lambda_f * di, di, p.c0_f[k]));
         }
     }
 }
@@ -88,12 +96,15 @@ struct Acc<kSpatial, F64> {
     }
     __device__ __forceinline__ float final(const SweepParams& p) const {
         // class representatives (du,dv) = (0,0),(1,0),(0,1),(1,1) -> k = 4,7,5,8
-        float r = best;
-        r = fminf(r, static_cast<float>(static_cast<double>(m[0]) + p.rho[4]));
-        r = fminf(r, static_cast<float>(static_cast<double>(m[1]) + p.rho[7]));
-        r = fminf(r, static_cast<float>(static_cast<double>(m[2]) + p.rho[5]));
-        r = fminf(r, static_cast<float>(static_cast<double>(m[3]) + p.rho[8]));
-        return r;
+        // Rounding to f32 is monotone, so the min of the f64 sums rounds to the
+        // min of the rounded sums: one F2F down instead of four (conversions
+        // run at a quarter of the FP32 rate).  No NaNs reach here.
+        const double s0 = static_cast<double>(m[0]) + p.rho[4];
+        const double s1 = static_cast<double>(m[1]) + p.rho[7];
+        const double s2 = static_cast<double>(m[2]) + p.rho[5];
+        const double s3 = static_cast<double>(m[3]) + p.rho[8];
+        const double a = s0 < s1 ? s0 : s1, b = s2 < s3 ? s2 : s3;
+        return fminf(best, static_cast<float>(a < b ? a : b));
     }
 };
 
@@ -200,6 +211,17 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 __device__ __forceinline__ void consumer_sync(int nthreads) {
     asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+// AND of `pred` over the consumer threads (named barrier 1, like consumer_sync).
+__device__ __forceinline__ bool consumer_all(bool pred, int nthreads) {
+    int r;
+    asm volatile(
+        "{\n\t.reg .pred p, q;\n\tsetp.ne.s32 p, %1, 0;\n\t"
+        "barrier.cta.red.and.pred q, 1, %2, p;\n\tselp.s32 %0, 1, 0, q;\n\t}"
+        : "=r"(r)
+        : "r"(static_cast<int>(pred)), "r"(nthreads)
+        : "memory");
+    return r != 0;
 }
 __device__ __forceinline__ void st_release_cta(int* p, int v) {
     asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
@@ -690,8 +712,12 @@ __global__ void __launch_bounds__((MW * NWU + 1) * 32, 1)
     // ======================= consumer warps =================================
     const int wu = w / nwv, wv = w - wu * nwv;
     const int vl = wv * kWV + kC * lane;
-    const bool full =
-        __all_sync(kFull, (c.u0 + wu * RW + RW <= p.nu) && (vl + kC <= p.nv));
+    // CTA-uniform: one partial warp makes every warp of the CTA take the masked
+    // variant.  Per-warp choice ran four role variants on one SM (TOP/BOT x
+    // full/partial, ~14 KB of SASS each) and the instruction cache thrashed
+    // (ncu: no_inst the top stall, 2.4x longer steps at W = 160).
+    const bool full = consumer_all((c.u0 + wu * RW + RW <= p.nu) && (vl + kC <= p.nv),
+                                   ncw * 32);
     const bool top = wu == 0, bot = wu == NWU - 1;
 #define GD_ROLE(T, B)                                                                      \
     if (top == T && bot == B) {                                                            \
@@ -744,25 +770,26 @@ int coresident(int nwv) {
     return per_sm * sms;
 }
 
-constexpr int kNST = 6;
-
-// Strip shapes (rows per warp RW, warp rows NWU, max warp columns MW): narrow
-// planes (<= 512 columns) run 2 warp rows of 2 rows (R = 4, 2 warps per
-// scheduler); R = 1 serves single-row planes (2D).  Wide planes (<= 2048
+// Strip shapes X(RW rows per warp, NWU warp rows, MW max warp columns, NST
+// ring stages).  R = RW * NWU rows per strip.  Narrow planes (<= 256 columns)
+// get tall strips (R = 8, 16) so a batch of small volumes keeps enough bytes in
+// flight per step; <= 512 columns run R = 4 as 2 warp rows of 2 rows (2 warps
+// per scheduler); R = 1 serves single-row planes (2D).  Wide planes (<= 2048
 // columns) trade registers for warps.
-#define GD_SWEEP_CASES(X) \
-    X(1, 1, 4) X(2, 1, 4) X(2, 2, 4) X(4, 2, 4) X(1, 1, 16) X(2, 1, 16) X(4, 1, 16)
+#define GD_SWEEP_CASES(X)                                                          \
+    X(1, 1, 2, 6) X(2, 1, 2, 6) X(2, 2, 2, 6) X(4, 2, 2, 6) X(4, 4, 2, 4)             \
+    X(1, 1, 4, 6) X(2, 1, 4, 6) X(2, 2, 4, 6) X(4, 2, 4, 6)                           \
+    X(1, 1, 16, 6) X(2, 1, 16, 6) X(4, 1, 16, 6)
 
-int width_class(int nwv) { return nwv <= 4 ? 4 : 16; }
+int width_class(int nwv) { return nwv <= 2 ? 2 : (nwv <= 4 ? 4 : 16); }
 
-// R -> (RW, NWU): 1 -> (1,1), 2 -> (2,1), 4 -> (2,2), 8 -> (4,2)
 template <int KIND, bool F64>
 cudaError_t dispatch_r(int R, const CUtensorMap& tm_d, const CUtensorMap& tm_i,
                        const SweepParams& p, cudaStream_t s) {
     const int mw = width_class(p.nwv);
-#define GD_CASE(RWW, NW, MM)                                         \
+#define GD_CASE(RWW, NW, MM, NS)                                     \
     if (R == RWW * NW && mw == MM)                                   \
-        return launch_one<KIND, F64, RWW, NW, kNST, MM>(tm_d, tm_i, p, s);
+        return launch_one<KIND, F64, RWW, NW, NS, MM>(tm_d, tm_i, p, s);
     GD_SWEEP_CASES(GD_CASE)
 #undef GD_CASE
     return cudaErrorInvalidValue;
@@ -771,8 +798,8 @@ cudaError_t dispatch_r(int R, const CUtensorMap& tm_d, const CUtensorMap& tm_i,
 template <int KIND, bool F64>
 int dispatch_cores(int R, int nwv) {
     const int mw = width_class(nwv);
-#define GD_CASE(RWW, NW, MM) \
-    if (R == RWW * NW && mw == MM) return coresident<KIND, F64, RWW, NW, kNST, MM>(nwv);
+#define GD_CASE(RWW, NW, MM, NS) \
+    if (R == RWW * NW && mw == MM) return coresident<KIND, F64, RWW, NW, NS, MM>(nwv);
     GD_SWEEP_CASES(GD_CASE)
 #undef GD_CASE
     return 0;
@@ -794,13 +821,12 @@ cudaError_t launch_sweep(int kind, bool f64, int R, const CUtensorMap& tm_d,
     }
 }
 
-size_t sweep_smem_bytes(int R, int nwv) {
-    switch (R) {
-        case 1: return Layout<1, 1, kNST>::smem_bytes(nwv);
-        case 2: return Layout<2, 1, kNST>::smem_bytes(nwv);
-        case 4: return Layout<2, 2, kNST>::smem_bytes(nwv);
-        case 8: return Layout<4, 2, kNST>::smem_bytes(nwv);
-    }
+int sweep_warp_rows(int R, int nwv) {
+    const int mw = width_class(nwv);
+#define GD_CASE(RWW, NW, MM, NS) \
+    if (R == RWW * NW && mw == MM) return NW;
+    GD_SWEEP_CASES(GD_CASE)
+#undef GD_CASE
     return 0;
 }
 

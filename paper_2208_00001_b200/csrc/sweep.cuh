@@ -86,7 +86,8 @@ struct SweepParams {
 // Host-side launch (defined in sweep.cu).  R = rows per strip.
 cudaError_t launch_sweep(int kind, bool f64, int R, const CUtensorMap& tm_d,
                          const CUtensorMap& tm_i, const SweepParams& p, cudaStream_t stream);
-size_t sweep_smem_bytes(int R, int nwv);
+// Warp rows (NWU) of the strip shape serving R rows at this width; 0 = none.
+int sweep_warp_rows(int R, int nwv);
 int sweep_max_coresident(int R, int nwv, int kind, bool f64);
 
 }  // namespace gdb

@@ -111,6 +111,24 @@ def test_batched_matches_per_volume(gd, oracle):
         assert bitwise_equal(g[b], r), b
 
 
+@pytest.mark.parametrize("lam", LAMBDAS)
+@pytest.mark.parametrize("shape", [(10, 70, 150), (6, 24, 100)])
+def test_batched_tall_strips(gd, oracle, lam, shape):
+    """Large batches of narrow volumes run tall strips (R = 16 / 8 rows per CTA,
+    partial last strip at 70 rows) so more volumes share one launch group."""
+    rng = np.random.default_rng(23)
+    B = 48
+    imgs = dyadic_image(rng, (B,) + shape)
+    masks = np.ones((B,) + shape, np.float32)
+    for b in range(B):
+        masks[b].reshape(-1)[rng.integers(0, masks[b].size)] = 0.0
+    sp = (1.0, 1.0, 2.5)
+    g = gd.generalized_geodesic_batched(imgs, masks, sp, lam, 1e10, 2)
+    for b in range(0, B, 7):
+        r = oracle.generalized_geodesic(imgs[b], masks[b], sp, lam, 1e10, 2)
+        _check(g[b], r, lam)
+
+
 @pytest.mark.parametrize("lam", [0.0, 1.0])
 def test_gsf(gd, oracle, lam):
     shape = (24, 32, 28)
