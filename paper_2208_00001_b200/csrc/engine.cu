@@ -301,7 +301,8 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
         const long long pv = (nu + cand - 1) / cand;
         if (mc <= 0 || pv > mc) continue;
         const long long groups = (w.B + mc / pv - 1) / (mc / pv);
-        const double rel = cand <= 4 ? 1.0 : (cand == 8 ? 1.4 : 2.0);
+        // measured per-step cost relative to R = 4 (B200, 64 x 256x256x160 batch)
+        const double rel = cand <= 4 ? 1.0 : (cand == 8 ? 2.0 : 3.8);
         double cost = static_cast<double>(groups) * rel;
         if (cand == r_env) cost = -1.0;  // tuning override (experiments)
         if (R == 0 || cost < best) {

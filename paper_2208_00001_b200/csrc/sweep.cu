@@ -118,6 +118,13 @@ constexpr bool kPackedIntensity = false;
 // than the earlier detection gains.
 constexpr bool kDualPoll = false;
 
+#ifndef GD_MINB2
+#define GD_MINB2 3  // R = 4 strips of <= 256 columns: 3 CTAs per SM (batches; measured 97 -> 81 ms)
+#endif
+#ifndef GD_EARLY_POLL
+#define GD_EARLY_POLL 0
+#endif
+
 // Cycle counters for diagnosis (built only with -DGD_SWEEP_TRACE).
 #ifdef GD_SWEEP_TRACE
 #define GD_T0(v) const long long v = clock64()
@@ -384,6 +391,23 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
     const float* sd_cur = sd_base;
     const float* si_cur = si_base;
 
+    auto load_row = [&](const unsigned long long* q, unsigned long long (&h)[6]) {
+        ld_tagged2(q, h[1], h[2]);
+        ld_tagged2(q + 64, h[3], h[4]);
+        h[0] = edge_l ? ld_tagged(q - 1) : 0ull;   // previous block, last word
+        h[5] = edge_r ? ld_tagged(q + 66) : 0ull;  // next block, first word
+    };
+    // First poll of the next step's halo rows (published at step j), issued
+    // GD_EARLY_POLL = 1: right after this strip publishes its own step-j rows,
+    // 2: just before the step barrier; 0: at the top of the next step.
+    unsigned long long huN[6], hdN[6];
+    auto early_poll = [&](int j) {
+        const int par = j & 1;
+        if (TOP && has_up) load_row(up0 + par * 2ll * VW, huN);
+        if (BOT && has_dn) load_row(dn0 + par * 2ll * VW, hdN);
+    };
+    if (GD_EARLY_POLL != 0 && J > 0) early_poll(0);
+
     // One relaxation step: plane j from the previous plane (Pin, Iin) into (Pout, Iout).
     auto step = [&](int j, const float (&Pin)[RW][kC], const float (&Iin)[RW][kC],
                     float (&Pout)[RW][kC], float (&Iout)[RW][kC]) {
@@ -406,13 +430,13 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
         // step, B after the strip's own rows are relaxed; the spin alternates
         // between them so a fresh word is seen within about half a round trip.
         unsigned long long huA[6], hdA[6], huB[6], hdB[6];  // [0] = v-1, [1..4] own, [5] = v+4
-        auto load_row = [&](const unsigned long long* q, unsigned long long (&h)[6]) {
-            ld_tagged2(q, h[1], h[2]);
-            ld_tagged2(q + 64, h[3], h[4]);
-            h[0] = edge_l ? ld_tagged(q - 1) : 0ull;   // previous block, last word
-            h[5] = edge_r ? ld_tagged(q + 66) : 0ull;  // next block, first word
-        };
-        if (!GD_DBG(4)) {
+        if (GD_EARLY_POLL != 0) {
+#pragma unroll
+            for (int i = 0; i < 6; ++i) {
+                huA[i] = huN[i];
+                hdA[i] = hdN[i];
+            }
+        } else if (!GD_DBG(4)) {
             if (TOP && has_up) load_row(hup, huA);
             if (BOT && has_dn) load_row(hdn, hdA);
         }
@@ -571,6 +595,7 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
         if (TOP) fin(0);
         if (BOT && (RW > 1 || !TOP)) fin(RW - 1);
         if (j < J) publish_halo(j, Pout);
+        if (GD_EARLY_POLL == 1 && j < J) early_poll(j);
 #pragma unroll
         for (int r = 0; r < RW; ++r)
             if (!((TOP && r == 0) || (BOT && r == RW - 1))) fin(r);
@@ -603,6 +628,7 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
         const bool near_turn = turn_fence && j <= n1 && j + NST >= n1;
         if (near_turn) fence_proxy_async_global();
 
+        if (GD_EARLY_POLL == 2 && j < J) early_poll(j);
         GD_T0(t_bar);
 #ifdef GD_SWEEP_TRACE
         if (TOP || BOT) trc[7] += t_bar - t_tail0_outer;
@@ -636,7 +662,7 @@ template <int KIND, bool F64, int RW, int NWU, int NST, int MW>
 // One CTA per SM: two R = 2 CTAs per SM (126-register cap) measured 1.66 vs
 // 1.25 us/step for R = 4 at 512^3 -- twice the halo links cost more than the
 // second CTA hides (profiles/README.md).
-__global__ void __launch_bounds__((MW * NWU + 1) * 32, 1)
+__global__ void __launch_bounds__((MW * NWU + 1) * 32, MW == 2 && NWU * RW == 4 ? GD_MINB2 : 1)
     sweep_kernel(const __grid_constant__ CUtensorMap tm_d, const __grid_constant__ CUtensorMap tm_i,
                  const __grid_constant__ SweepParams p) {
     using L = Layout<RW, NWU, NST>;

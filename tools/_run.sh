@@ -1,1 +1,5 @@
-python -m pytest tests -m gpu -x -q 2>&1 | tail -2; GEODIST_TIME_LOG=1 python tools/time_configs.py --only probe > gpurun_out/cfg6.txt 2>&1; python tools/time_configs.py --only batch >> gpurun_out/cfg6.txt 2>&1
+for v in _mb3 _mb4 _mb3ep2; do
+  echo "== variant '$v'"
+  GEODIST_LIB=paper_2208_00001_b200/lib/libgeodist_b200$v.so python tools/time_configs.py --only batch64_256
+  GEODIST_LIB=paper_2208_00001_b200/lib/libgeodist_b200$v.so python tools/time_configs.py --only gsf
+done > gpurun_out/mb.txt 2>&1
