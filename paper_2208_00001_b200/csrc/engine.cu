@@ -375,7 +375,7 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
         sc.tag += static_cast<uint32_t>(J + 1);
         // Diagnostic cycle counters: only a -DGD_SWEEP_TRACE build writes them.
         static const bool trace_on = std::getenv("GEODIST_SWEEP_TRACE") != nullptr;
-        const size_t trace_n = static_cast<size_t>(nvol) * per_vol * 64 * 8;
+        const size_t trace_n = static_cast<size_t>(nvol) * per_vol * 64 * 12;
         if (trace_on) {
             GD_ST(sc.trace.ensure(trace_n * sizeof(long long)));
             GD_CK(cudaMemsetAsync(sc.trace.p, 0, trace_n * sizeof(long long), s));
@@ -396,22 +396,23 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
             GD_CK(cudaStreamSynchronize(s));
             const int nw = nwv * sweep_warp_rows(R, nwv);
             for (int w = 0; w < nw; ++w) {
-                double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                double acc[12] = {};
                 long long n = 0;
                 for (long long cta = 0; cta < nvol * per_vol; ++cta) {
-                    const long long* o = &h[(cta * 64 + w) * 8];
+                    const long long* o = &h[(cta * 64 + w) * 12];
                     if (o[5] == 0) continue;
-                    for (int k = 0; k < 8; ++k) acc[k] += o[k];
+                    for (int k = 0; k < 12; ++k) acc[k] += o[k];
                     ++n;
                 }
                 if (!n) continue;
                 const double steps = acc[5] / n;
+                auto a = [&](int k) { return acc[k] / n / steps; };
                 std::fprintf(stderr,
-                             "trace axis=%d R=%d maxc=%d warp=%d: cycles/step total %.0f tma %.0f spin %.0f "
-                             "barrier %.0f reloads/step %.2f phaseA %.0f tail %.0f (ctas %lld)\n",
-                             axis, R, maxc, w, acc[4] / n / steps, acc[0] / n / steps, acc[1] / n / steps,
-                             acc[2] / n / steps, acc[3] / n / steps, acc[6] / n / steps,
-                             acc[7] / n / steps, n);
+                             "trace axis=%d R=%d maxc=%d warp=%d: cycles/step total %.0f pre %.0f tma %.0f "
+                             "phaseA %.0f spin %.0f crit %.0f tail %.0f barrier %.0f post %.0f "
+                             "reloads/step %.2f (ctas %lld)\n",
+                             axis, R, maxc, w, a(4), a(8), a(0), a(6), a(1), a(9), a(7), a(2), a(10),
+                             a(3), n);
             }
         }
         ++g_launches;

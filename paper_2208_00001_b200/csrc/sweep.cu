@@ -116,8 +116,14 @@ constexpr bool kPackedIntensity = false;
 // Second halo poll issued mid-step (alternating spin).  Measured slower on
 // B200 (1.48 vs 1.24 us/step at 512^2): the extra loads and registers cost more
 // than the earlier detection gains.
-constexpr bool kDualPoll = false;
+#ifndef GD_DUAL_POLL
+#define GD_DUAL_POLL 0
+#endif
+constexpr bool kDualPoll = GD_DUAL_POLL != 0;
 
+#ifndef GD_NST4
+#define GD_NST4 6
+#endif
 #ifndef GD_MINB2
 #define GD_MINB2 3  // R = 4 strips of <= 256 columns: 3 CTAs per SM (batches; measured 97 -> 81 ms)
 #endif
@@ -353,7 +359,7 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
 
     float PA[RW][kC], IA[RW][kC], PB[RW][kC], IB[RW][kC];
 #ifdef GD_SWEEP_TRACE
-    long long trc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // tma, spin, barrier, reloads, total, steps, phaseA, tail
+    long long trc[12] = {};  // tma, spin, barrier, reloads, total, steps, phaseA, tail, pre, crit, post, -
     const long long t_begin = clock64();
 #endif
 
@@ -411,6 +417,7 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
     // One relaxation step: plane j from the previous plane (Pin, Iin) into (Pout, Iout).
     auto step = [&](int j, const float (&Pin)[RW][kC], const float (&Iin)[RW][kC],
                     float (&Pout)[RW][kC], float (&Iout)[RW][kC]) {
+        GD_T0(t_entry);
         const int pslot = slot;
         const float* sip = si_cur;  // previous plane's I box
         if (++slot == NST) {
@@ -429,18 +436,17 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
         // Two polls of each halo window are kept in flight: A at the top of the
         // step, B after the strip's own rows are relaxed; the spin alternates
         // between them so a fresh word is seen within about half a round trip.
-        unsigned long long huA[6], hdA[6], huB[6], hdB[6];  // [0] = v-1, [1..4] own, [5] = v+4
-        if (GD_EARLY_POLL != 0) {
-#pragma unroll
-            for (int i = 0; i < 6; ++i) {
-                huA[i] = huN[i];
-                hdA[i] = hdN[i];
-            }
-        } else if (!GD_DBG(4)) {
+        // [0] = v-1, [1..4] own, [5] = v+4.  Poll A lives in huN/hdN (no copy:
+        // a register copy of an in-flight load would stall right there).
+        unsigned long long(&huA)[6] = huN;
+        unsigned long long(&hdA)[6] = hdN;
+        unsigned long long huB[6], hdB[6];
+        if (GD_EARLY_POLL == 0 && !GD_DBG(4)) {
             if (TOP && has_up) load_row(hup, huA);
             if (BOT && has_dn) load_row(hdn, hdA);
         }
 
+        GD_TADD(8, t_entry);
         GD_T0(t_tma);
         mbar_wait(&c.full[slot], phase);
         GD_TADD(0, t_tma);
@@ -595,6 +601,9 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
         if (TOP) fin(0);
         if (BOT && (RW > 1 || !TOP)) fin(RW - 1);
         if (j < J) publish_halo(j, Pout);
+#ifdef GD_SWEEP_TRACE
+        if (TOP || BOT) trc[9] += clock64() - t_tail0_outer;
+#endif
         if (GD_EARLY_POLL == 1 && j < J) early_poll(j);
 #pragma unroll
         for (int r = 0; r < RW; ++r)
@@ -635,7 +644,9 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
 #endif
         consumer_sync(nthreads);
         GD_TADD(2, t_bar);
+        GD_T0(t_post);
         if (tid == 0 && near_turn) st_release_cta(c.progress, j);
+        GD_TADD(10, t_post);
     };
 
     int j = 1;
@@ -648,8 +659,8 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
     trc[4] = clock64() - t_begin;
     trc[5] = J;
     if (p.trace && lane == 0) {
-        long long* o = p.trace + (static_cast<long long>(c.g) * 64 + wu * nwv + wv) * 8;
-        for (int i = 0; i < 8; ++i) o[i] = trc[i];
+        long long* o = p.trace + (static_cast<long long>(c.g) * 64 + wu * nwv + wv) * 12;
+        for (int i = 0; i < 12; ++i) o[i] = trc[i];
     }
 #endif
 }
@@ -804,7 +815,7 @@ int coresident(int nwv) {
 // columns) trade registers for warps.
 #define GD_SWEEP_CASES(X)                                                          \
     X(1, 1, 2, 6) X(2, 1, 2, 6) X(2, 2, 2, 6) X(4, 2, 2, 6) X(4, 4, 2, 4)             \
-    X(1, 1, 4, 6) X(2, 1, 4, 6) X(2, 2, 4, 6) X(4, 2, 4, 6)                           \
+    X(1, 1, 4, 6) X(2, 1, 4, 6) X(2, 2, 4, GD_NST4) X(4, 2, 4, 6)                     \
     X(1, 1, 16, 6) X(2, 1, 16, 6) X(4, 1, 16, 6)
 
 int width_class(int nwv) { return nwv <= 2 ? 2 : (nwv <= 4 ? 4 : 16); }

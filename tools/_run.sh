@@ -1,8 +1,2 @@
-set -x
-python bench.py --steps 20 --warmup 3 > gpurun_out/bench_r01b.json 2> gpurun_out/bench_r01b.err || exit 1
-python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/ref_r01b.json 2> gpurun_out/ref_r01b.err
-python tools/prof_step.py --reps 1 > /dev/null 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r01b.csv python tools/prof_step.py --reps 1 > gpurun_out/ncu_l.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:sweep_kernel -c 1 -o gpurun_out/prof_r01b_sweep -f python tools/prof_step.py --reps 1 > gpurun_out/ncu_s.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:transpose -c 1 -o gpurun_out/prof_r01b_transpose -f python tools/prof_step.py --reps 1 > gpurun_out/ncu_t.log 2>&1
-tail -2 gpurun_out/ncu_s.log
+for v in "" _tb2; do echo "== $v"; GEODIST_LIB=paper_2208_00001_b200/lib/libgeodist_b200$v.so python tools/time_configs.py --only 3d_512_l1; done > gpurun_out/tb2.txt 2>&1
+GEODIST_LIB=paper_2208_00001_b200/lib/libgeodist_b200_tb2.so python -m pytest tests/test_parity_gpu.py -x -q 2>&1 | tail -5 >> gpurun_out/tb2.txt
