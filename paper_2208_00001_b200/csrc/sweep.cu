@@ -3,6 +3,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <type_traits>
 
 #include "sweep.cuh"
 
@@ -113,22 +114,16 @@ struct Acc<kSpatial, F64> {
 // instructions per voxel); the scalar FADD with an |operand| is cheaper.
 constexpr bool kPackedIntensity = false;
 
-// Second halo poll issued mid-step (alternating spin).  Measured slower on
-// B200 (1.48 vs 1.24 us/step at 512^2): the extra loads and registers cost more
-// than the earlier detection gains.
-#ifndef GD_DUAL_POLL
-#define GD_DUAL_POLL 0
-#endif
-constexpr bool kDualPoll = GD_DUAL_POLL != 0;
+// Halo polls: one per step, issued at the top of the step.  Measured slower on
+// B200 at 512^3: a second poll in flight mid-step (1.48 vs 1.24 us/step: more
+// L2 requests), and issuing the poll at the end of the previous step (after the
+// publish: 1.17 vs 1.09 us/step, the poll is stale more often).
 
 #ifndef GD_NST4
 #define GD_NST4 6
 #endif
 #ifndef GD_MINB2
 #define GD_MINB2 3  // R = 4 strips of <= 256 columns: 3 CTAs per SM (batches; measured 97 -> 81 ms)
-#endif
-#ifndef GD_EARLY_POLL
-#define GD_EARLY_POLL 0
 #endif
 
 // Cycle counters for diagnosis (built only with -DGD_SWEEP_TRACE).
@@ -175,16 +170,23 @@ __device__ __forceinline__ void relax_row(Acc<KIND, F64> (&acc)[kC], const float
     }
 }
 
-template <int RW, int NWU, int NST>
+// TB (temporal blocking over plane pairs): the boxes carry one ghost row above
+// and below the strip for the distances and two for the intensities, and the
+// halo carries two rows per side, exchanged once per two planes.
+template <int RW, int NWU, int NST, bool TB>
 struct Layout {
     static constexpr int R = RW * NWU;                            // rows per strip
-    static constexpr int DBOX = R * kWV;                          // floats per column-block box
-    static constexpr int IBOX = ((R + 2) * kIW + 31) / 32 * 32;   // 128-B aligned slot stride
-    static constexpr int IBYTES = (R + 2) * kIW * 4;
+    static constexpr int DOFF = TB ? 1 : 0;                       // box row of strip row 0 (d)
+    static constexpr int IOFF = TB ? 2 : 1;                       // box row of strip row 0 (I)
+    static constexpr int HROWS = TB ? 2 : 1;                      // halo rows per side
+    static constexpr int ESL = RW + (TB ? 1 : 0);                 // edge slots per side (+ ghost)
+    static constexpr int DBOX = (R + 2 * DOFF) * kWV;             // floats per column-block box
+    static constexpr int IBOX = ((R + 2 * IOFF) * kIW + 31) / 32 * 32;  // 128-B aligned stride
+    static constexpr int IBYTES = (R + 2 * IOFF) * kIW * 4;
     static size_t smem_bytes(int nwv) {
         return static_cast<size_t>(NST) * nwv * (DBOX + IBOX) * 4     // TMA ring
                + static_cast<size_t>(2) * NWU * 2 * nwv * kWV * 4     // warp-row boundary rows
-               + static_cast<size_t>(2) * NWU * nwv * 2 * RW * 4      // warp-edge columns
+               + static_cast<size_t>(2) * NWU * nwv * 2 * ESL * 4     // warp-edge columns
                + 2 * NST * 8 + 16 + 128;                              // barriers, progress
     }
 };
@@ -246,7 +248,7 @@ __device__ __forceinline__ int ld_acquire_cta(const int* p) {
 }
 
 // Shared-memory carve-up and launch geometry, common to producer and consumers.
-template <int RW, int NWU, int NST>
+template <int RW, int NWU, int NST, bool TB>
 struct Ctx {
     float* sd;          // [NST][nwv][R][128]      old distances (TMA)
     float* si;          // [NST][nwv][R+2][136]    intensities + row halo (TMA)
@@ -258,8 +260,9 @@ struct Ctx {
     int nwv, g, b, tu, u0, n1, J, VW;
 };
 
-template <int RW, int NWU, int NST>
-__device__ __forceinline__ int plane_of(const SweepParams& p, const Ctx<RW, NWU, NST>& c, int j) {
+template <int RW, int NWU, int NST, bool TB>
+__device__ __forceinline__ int plane_of(const SweepParams& p, const Ctx<RW, NWU, NST, TB>& c,
+                                        int j) {
     if (j <= c.n1) return p.first_orient > 0 ? j : c.n1 - j;
     const int k = j - c.n1;
     return p.first_orient > 0 ? c.n1 - k : k;
@@ -268,10 +271,12 @@ __device__ __forceinline__ int plane_of(const SweepParams& p, const Ctx<RW, NWU,
 // One consumer warp's whole sweep.  TOP / BOT: the warp row borders the strip
 // above / below (tagged global halo); FULL: every voxel of the warp is inside
 // the volume.  Specialising on the role keeps the per-step body branch-free.
-template <int KIND, bool F64, int RW, int NWU, int NST, bool TOP, bool BOT, bool FULL>
-__device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW, NWU, NST>& c,
-                                              int wu, int wv, int lane) {
-    using L = Layout<RW, NWU, NST>;
+template <int KIND, bool F64, int RW, int NWU, int NST, bool TB, bool TOP, bool BOT, bool FULL>
+__device__ __forceinline__ void consumer_loop(const SweepParams& p,
+                                              const Ctx<RW, NWU, NST, TB>& c, int wu, int wv,
+                                              int lane) {
+    using L = Layout<RW, NWU, NST, TB>;
+    static_assert(!TB || RW >= 2, "temporal blocking publishes two rows per border warp");
     constexpr int R = L::R, DBOX = L::DBOX, IBOX = L::IBOX;
     constexpr bool kI = KIND != kSpatial;
     const int nwv = c.nwv, VW = c.VW, J = c.J, n1 = c.n1;
@@ -283,8 +288,12 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
     const uint32_t tag_base = p.tag_base;
     const bool turn_fence = p.fence_turn != 0;
 
+    constexpr int DOFF = L::DOFF, IOFF = L::IOFF, HROWS = L::HROWS, ESL = L::ESL;
+    static_assert(!TB || NWU >= 2, "temporal blocking keeps one ghost row per border warp");
     const bool has_up = TOP && c.tu > 0, has_dn = BOT && c.tu + 1 < p.ntu;
-    const long long strip_words = 2ll * 2 * VW;  // per strip: 2 parities x {TOP, BOT}
+    // per strip: 2 parities x {TOP rows, BOT rows} x HROWS rows of VW words
+    const long long strip_words = 2ll * 2 * HROWS * VW;
+    const long long PARW = 2ll * HROWS * VW;
     const long long strip0 = static_cast<long long>(c.b) * p.ntu;
     // Halo row layout (per warp column block of 128 words): columns q = 0,1 of
     // all 32 lanes, then q = 2,3 -- lane l owns words 2l, 2l+1, 64+2l, 65+2l, so
@@ -294,17 +303,19 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
     const bool has_left = vl > 0, has_right = vl + kC < p.nv;
     const bool edge_l = lane == 0 && has_left, edge_r = lane == 31 && has_right;
     const int hl = wv * kWV + 2 * lane;
-    const unsigned long long* up0 = p.halo + (strip0 + c.tu - 1) * strip_words + VW + hl;
+    // the neighbour above publishes its last HROWS rows, the one below its first
+    const unsigned long long* up0 =
+        p.halo + (strip0 + c.tu - 1) * strip_words + HROWS * VW + hl;
     const unsigned long long* dn0 = p.halo + (strip0 + c.tu + 1) * strip_words + hl;
     unsigned long long* self0 = p.halo + static_cast<long long>(c.g) * strip_words + hl;
     const bool pub_up = TOP && c.tu > 0, pub_dn = BOT && c.tu + 1 < p.ntu;
-    // neighbour-warp edge columns
-    const int eoffL = ((wu * nwv + wv - 1) * 2 + 1) * RW;
-    const int eoffR = ((wu * nwv + wv + 1) * 2 + 0) * RW;
+    // neighbour-warp edge columns (ESL slots per side: own rows, then the ghost row)
+    const int eoffL = ((wu * nwv + wv - 1) * 2 + 1) * ESL;
+    const int eoffR = ((wu * nwv + wv + 1) * 2 + 0) * ESL;
     const bool wl = wv > 0, wr = wv + 1 < nwv;
-    float* const edge_own = c.edge + (wu * nwv + wv) * 2 * RW;
-    const int EPAR = NWU * nwv * 2 * RW;  // edge buffer parity stride
-    const int RPAR = NWU * 2 * VW;        // rows buffer parity stride
+    float* const edge_own = c.edge + (wu * nwv + wv) * 2 * ESL;
+    const int EPAR = NWU * nwv * 2 * ESL;  // edge buffer parity stride
+    const int RPAR = NWU * 2 * VW;         // rows buffer parity stride
 
     bool rowv[RW], colv[kC];
 #pragma unroll
@@ -324,18 +335,34 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
     const float* const si_base = c.si + wv * IBOX;
     const int SD_STRIDE = nwv * DBOX, SI_STRIDE = nwv * IBOX;
 
+    // TB ghost scratch: the ghost row of every forward A step, read back as the
+    // ghost's old distance in the backward pass (this warp's own earlier stores:
+    // no cross-CTA visibility question).  [cta][TOP|BOT][forward step / 2][VW].
+    const int gsteps = c.n1 / 2 + 1;
+    float* const gscr = TB ? p.ghost + ((static_cast<long long>(c.g) * 2 + (TOP ? 0 : 1)) *
+                                            gsteps) * VW + vl
+                           : nullptr;
+
+    // Halo publication: TOP rows 0..HROWS-1, BOT rows RW-HROWS..RW-1.
     auto publish_halo = [&](int j, const float (&N)[RW][kC]) {
-        const int par = j & 1;
+        const int par = TB ? (j >> 1) & 1 : j & 1;
         const uint32_t tag = tag_base + static_cast<uint32_t>(j);
-        unsigned long long* q = self0 + par * 2ll * VW;
+        unsigned long long* q = self0 + par * PARW;
         if (GD_DBG(2)) return;
         if (pub_up) {
-            st_tagged2(q, N[0][0], N[0][1], tag);
-            st_tagged2(q + 64, N[0][2], N[0][3], tag);
+#pragma unroll
+            for (int k = 0; k < HROWS; ++k) {
+                st_tagged2(q + k * VW, N[k][0], N[k][1], tag);
+                st_tagged2(q + k * VW + 64, N[k][2], N[k][3], tag);
+            }
         }
         if (pub_dn) {
-            st_tagged2(q + VW, N[RW - 1][0], N[RW - 1][1], tag);
-            st_tagged2(q + VW + 64, N[RW - 1][2], N[RW - 1][3], tag);
+#pragma unroll
+            for (int k = 0; k < HROWS; ++k) {
+                const int r = RW - HROWS + k;
+                st_tagged2(q + (HROWS + k) * VW, N[r][0], N[r][1], tag);
+                st_tagged2(q + (HROWS + k) * VW + 64, N[r][2], N[r][3], tag);
+            }
         }
     };
     auto publish_smem = [&](int j, const float (&N)[RW][kC]) {
@@ -353,11 +380,14 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
 #pragma unroll
         for (int r = 0; r < RW; ++r) {
             if (lane == 0) e[r] = N[r][0];
-            if (lane == 31) e[RW + r] = N[r][kC - 1];
+            if (lane == 31) e[ESL + r] = N[r][kC - 1];
         }
     };
 
     float PA[RW][kC], IA[RW][kC], PB[RW][kC], IB[RW][kC];
+    float G[kC];  // TB: ghost row (above for TOP, below for BOT) of the last A step
+#pragma unroll
+    for (int q = 0; q < kC; ++q) G[q] = INF;
 #ifdef GD_SWEEP_TRACE
     long long trc[12] = {};  // tma, spin, barrier, reloads, total, steps, phaseA, tail, pre, crit, post, -
     const long long t_begin = clock64();
@@ -369,11 +399,11 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
 #pragma unroll
         for (int r = 0; r < RW; ++r) {
             const float4 d4 =
-                *reinterpret_cast<const float4*>(sd_base + (r0 + r) * kWV + kC * lane);
+                *reinterpret_cast<const float4*>(sd_base + (r0 + r + DOFF) * kWV + kC * lane);
             PA[r][0] = d4.x; PA[r][1] = d4.y; PA[r][2] = d4.z; PA[r][3] = d4.w;
             if (kI) {
-                const float4 i4 = *reinterpret_cast<const float4*>(si_base + (r0 + r + 1) * kIW +
-                                                                   4 + kC * lane);
+                const float4 i4 = *reinterpret_cast<const float4*>(
+                    si_base + (r0 + r + IOFF) * kIW + 4 + kC * lane);
                 IA[r][0] = i4.x; IA[r][1] = i4.y; IA[r][2] = i4.z; IA[r][3] = i4.w;
             } else {
 #pragma unroll
@@ -403,20 +433,17 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
         h[0] = edge_l ? ld_tagged(q - 1) : 0ull;   // previous block, last word
         h[5] = edge_r ? ld_tagged(q + 66) : 0ull;  // next block, first word
     };
-    // First poll of the next step's halo rows (published at step j), issued
-    // GD_EARLY_POLL = 1: right after this strip publishes its own step-j rows,
-    // 2: just before the step barrier; 0: at the top of the next step.
-    unsigned long long huN[6], hdN[6];
-    auto early_poll = [&](int j) {
-        const int par = j & 1;
-        if (TOP && has_up) load_row(up0 + par * 2ll * VW, huN);
-        if (BOT && has_dn) load_row(dn0 + par * 2ll * VW, hdN);
-    };
-    if (GD_EARLY_POLL != 0 && J > 0) early_poll(0);
 
-    // One relaxation step: plane j from the previous plane (Pin, Iin) into (Pout, Iout).
-    auto step = [&](int j, const float (&Pin)[RW][kC], const float (&Iin)[RW][kC],
+    // One relaxation step: plane j from the previous plane (Pin, Iin) into
+    // (Pout, Iout).  kA: with TB, odd steps ("A") wait for the neighbours' two
+    // rows and also relax this warp's ghost row; even steps ("B") take the
+    // ghost row from registers and publish.  Without TB every step polls.
+    auto step = [&](auto kA, int j, const float (&Pin)[RW][kC], const float (&Iin)[RW][kC],
                     float (&Pout)[RW][kC], float (&Iout)[RW][kC]) {
+        constexpr bool A = decltype(kA)::value;
+        constexpr bool POLL = !TB || A;    // this step reads the tagged halo
+        constexpr bool GHOST = TB && A;    // this step relaxes the ghost row
+        constexpr bool USEG = TB && !A;    // this step takes the ghost row as a neighbour
         GD_T0(t_entry);
         const int pslot = slot;
         const float* sip = si_cur;  // previous plane's I box
@@ -429,22 +456,25 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
             sd_cur += SD_STRIDE;
             si_cur += SI_STRIDE;
         }
-        const int par = (j - 1) & 1;
+        const int par = (j - 1) & 1;  // smem (rows / edge) parity of the previous plane
+        const int hpar = TB ? ((j - 1) >> 1) & 1 : (j - 1) & 1;
         const uint32_t want = tag_base + static_cast<uint32_t>(j - 1);
-        const unsigned long long* hup = up0 + par * 2ll * VW;
-        const unsigned long long* hdn = dn0 + par * 2ll * VW;
-        // Two polls of each halo window are kept in flight: A at the top of the
-        // step, B after the strip's own rows are relaxed; the spin alternates
-        // between them so a fresh word is seen within about half a round trip.
-        // [0] = v-1, [1..4] own, [5] = v+4.  Poll A lives in huN/hdN (no copy:
-        // a register copy of an in-flight load would stall right there).
-        unsigned long long(&huA)[6] = huN;
-        unsigned long long(&hdA)[6] = hdN;
-        unsigned long long huB[6], hdB[6];
-        if (GD_EARLY_POLL == 0 && !GD_DBG(4)) {
-            if (TOP && has_up) load_row(hup, huA);
-            if (BOT && has_dn) load_row(hdn, hdA);
+        const unsigned long long* hup = up0 + hpar * PARW;
+        const unsigned long long* hdn = dn0 + hpar * PARW;
+        // [k][0] = v-1, [k][1..4] own, [k][5] = v+4
+        unsigned long long hu[HROWS][6], hd[HROWS][6];
+        if (POLL && !GD_DBG(4)) {
+#pragma unroll
+            for (int k = 0; k < HROWS; ++k) {
+                if (TOP && has_up) load_row(hup + k * VW, hu[k]);
+                if (BOT && has_dn) load_row(hdn + k * VW, hd[k]);
+            }
         }
+        const bool backward = j > n1;
+        const int gslot = (2 * n1 - j) >> 1;  // backward A step: forward step 2 n1 - j
+        float4 gold = make_float4(INF, INF, INF, INF);
+        if (GHOST && backward && (TOP ? has_up : has_dn))
+            gold = *reinterpret_cast<const float4*>(gscr + static_cast<long long>(gslot) * VW);
 
         GD_TADD(8, t_entry);
         GD_T0(t_tma);
@@ -454,12 +484,12 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
         float dold[RW][kC], ic[RW][kC];
 #pragma unroll
         for (int r = 0; r < RW; ++r) {
-            const float4 d4 =
-                *reinterpret_cast<const float4*>(sd_cur + (r0 + r) * kWV + kC * lane);
+            const float4 d4 = *reinterpret_cast<const float4*>(sd_cur + (r0 + r + DOFF) * kWV +
+                                                               kC * lane);
             dold[r][0] = d4.x; dold[r][1] = d4.y; dold[r][2] = d4.z; dold[r][3] = d4.w;
             if (kI) {
-                const float4 i4 = *reinterpret_cast<const float4*>(si_cur + (r0 + r + 1) * kIW +
-                                                                   4 + kC * lane);
+                const float4 i4 = *reinterpret_cast<const float4*>(
+                    si_cur + (r0 + r + IOFF) * kIW + 4 + kC * lane);
                 ic[r][0] = i4.x; ic[r][1] = i4.y; ic[r][2] = i4.z; ic[r][3] = i4.w;
             } else {
 #pragma unroll
@@ -475,9 +505,33 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
 #pragma unroll
             for (int q = 0; q < kC; ++q) acc[r][q].init(dold[r][q]);
 
+        // Ghost row (GHOST steps): strip row -1 (TOP) or R (BOT) of plane j.
+        // Its old distance: the TMA box in the forward pass; in the backward
+        // pass the forward ghost of the same plane from the scratch (the box row
+        // is another CTA's forward output, not ordered before this TMA read).
+        constexpr int gr = TOP ? -1 : R;
+        Acc<KIND, F64> accG[kC];
+        float ig[kC];
+        if (GHOST) {
+            const float4 d4 = *reinterpret_cast<const float4*>(sd_cur + (gr + DOFF) * kWV +
+                                                               kC * lane);
+            const float gd[kC] = {d4.x, d4.y, d4.z, d4.w};
+            const float gb[kC] = {gold.x, gold.y, gold.z, gold.w};
+#pragma unroll
+            for (int q = 0; q < kC; ++q) accG[q].init(backward ? gb[q] : gd[q]);
+            if (kI) {
+                const float4 i4 = *reinterpret_cast<const float4*>(
+                    si_cur + (gr + IOFF) * kIW + 4 + kC * lane);
+                ig[0] = i4.x; ig[1] = i4.y; ig[2] = i4.z; ig[3] = i4.w;
+            } else {
+#pragma unroll
+                for (int q = 0; q < kC; ++q) ig[q] = 0.0f;
+            }
+        }
+
         auto i_window = [&](int sr, float (&iw)[6]) {
             if (kI) {
-                const float* rp = sip + (sr + 1) * kIW;
+                const float* rp = sip + (sr + IOFF) * kIW;
                 const float4 i4 = *reinterpret_cast<const float4*>(rp + 4 + kC * lane);
                 const float c4[kC] = {i4.x, i4.y, i4.z, i4.w};
                 make_window(c4, rp[3], rp[4 + kWV], lane, iw);
@@ -495,7 +549,7 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
             const float eR = wr ? edge_prev[eoffR + k] : INF;
             make_window(Pin[k], eL, eR, lane, pw);
             if (kI) {
-                const float* rp = sip + (r0 + k + 1) * kIW;
+                const float* rp = sip + (r0 + k + IOFF) * kIW;
                 make_window(Iin[k], rp[3], rp[4 + kWV], lane, iw);
             } else {
 #pragma unroll
@@ -504,10 +558,8 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
             if (k - 1 >= 0) relax_row<KIND, F64>(acc[k - 1], pw, iw, ic[k - 1], +1, p);
             relax_row<KIND, F64>(acc[k], pw, iw, ic[k], 0, p);
             if (k + 1 < RW) relax_row<KIND, F64>(acc[k + 1], pw, iw, ic[k + 1], -1, p);
-        }
-        if (kDualPoll) {
-            if (TOP && has_up) load_row(hup, huB);
-            if (BOT && has_dn) load_row(hdn, hdB);
+            if (GHOST && TOP && k == 0) relax_row<KIND, F64>(accG, pw, iw, ig, +1, p);
+            if (GHOST && BOT && k == RW - 1) relax_row<KIND, F64>(accG, pw, iw, ig, -1, p);
         }
         if (!TOP) {
             const float* rp = rows_prev + ((wu - 1) * 2 + 1) * VW;  // last row of warp row wu-1
@@ -527,12 +579,21 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
             i_window(r0 + RW, iw);
             relax_row<KIND, F64>(acc[RW - 1], pw, iw, ic[RW - 1], +1, p);
         }
+        // B steps: the row outside the strip is the ghost relaxed at the A step.
+        if (USEG && (TOP ? has_up : has_dn)) {
+            float pw[6], iw[6];
+            make_window(G, wl ? edge_prev[eoffL + RW] : INF, wr ? edge_prev[eoffR + RW] : INF,
+                        lane, pw);
+            i_window(gr, iw);
+            if (TOP) relax_row<KIND, F64>(acc[0], pw, iw, ic[0], -1, p);
+            else relax_row<KIND, F64>(acc[RW - 1], pw, iw, ic[RW - 1], +1, p);
+        }
 
         // ---- phase B: rows above / below the strip (tagged halo) -------------
 #ifdef GD_SWEEP_TRACE
         long long t_tail0_outer = 0;
 #endif
-        if (TOP || BOT) {
+        if (POLL && (TOP || BOT)) {
             auto fresh = [&](const unsigned long long (&h)[6]) {
                 bool ok = (!edge_l || tag_of(h[0]) == want) && (!edge_r || tag_of(h[5]) == want);
 #pragma unroll
@@ -542,47 +603,53 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
             long long spins = 0;
             GD_TADD(6, t_pa);
             GD_T0(t_spin);
-            bool useB = false;
             while (!GD_DBG(1)) {
-                const bool ok = useB ? ((!(TOP && has_up) || fresh(huB)) &&
-                                        (!(BOT && has_dn) || fresh(hdB)))
-                                     : ((!(TOP && has_up) || fresh(huA)) &&
-                                        (!(BOT && has_dn) || fresh(hdA)));
-                if (__all_sync(kFull, ok)) break;
-                if (useB) {
-                    if (TOP && has_up) load_row(hup, huB);
-                    if (BOT && has_dn) load_row(hdn, hdB);
-                } else {
-                    if (TOP && has_up) load_row(hup, huA);
-                    if (BOT && has_dn) load_row(hdn, hdA);
+                bool ok = true;
+#pragma unroll
+                for (int k = 0; k < HROWS; ++k) {
+                    if (TOP && has_up) ok = ok && fresh(hu[k]);
+                    if (BOT && has_dn) ok = ok && fresh(hd[k]);
                 }
-                if (kDualPoll) useB = !useB;
+                if (__all_sync(kFull, ok)) break;
+#pragma unroll
+                for (int k = 0; k < HROWS; ++k) {
+                    if (TOP && has_up) load_row(hup + k * VW, hu[k]);
+                    if (BOT && has_dn) load_row(hdn + k * VW, hd[k]);
+                }
                 if (++spins > kSpinLimit) __trap();
             }
             GD_TADD(1, t_spin);
 #ifdef GD_SWEEP_TRACE
             t_tail0_outer = clock64();
-#endif
-#ifdef GD_SWEEP_TRACE
             trc[3] += spins;
 #endif
-            unsigned long long hu[6], hd[6];
-#pragma unroll
-            for (int i = 0; i < 6; ++i) {
-                hu[i] = useB ? huB[i] : huA[i];
-                hd[i] = useB ? hdB[i] : hdA[i];
-            }
             if (TOP) {
-                float pw[6], iw[6];
-                halo_window(hu, has_up, has_left, has_right, lane, pw);
-                i_window(-1, iw);
-                relax_row<KIND, F64>(acc[0], pw, iw, ic[0], -1, p);
+                // rows -HROWS .. -1: the neighbour above's last rows
+                float pw1[6], iw1[6];
+                halo_window(hu[HROWS - 1], has_up, has_left, has_right, lane, pw1);
+                i_window(-1, iw1);
+                relax_row<KIND, F64>(acc[0], pw1, iw1, ic[0], -1, p);
+                if (GHOST && has_up) {
+                    float pw2[6], iw2[6];
+                    halo_window(hu[0], has_up, has_left, has_right, lane, pw2);
+                    i_window(-2, iw2);
+                    relax_row<KIND, F64>(accG, pw2, iw2, ig, -1, p);
+                    relax_row<KIND, F64>(accG, pw1, iw1, ig, 0, p);
+                }
             }
             if (BOT) {
-                float pw[6], iw[6];
-                halo_window(hd, has_dn, has_left, has_right, lane, pw);
-                i_window(R, iw);
-                relax_row<KIND, F64>(acc[RW - 1], pw, iw, ic[RW - 1], +1, p);
+                // rows R .. R+HROWS-1: the neighbour below's first rows
+                float pw1[6], iw1[6];
+                halo_window(hd[0], has_dn, has_left, has_right, lane, pw1);
+                i_window(R, iw1);
+                relax_row<KIND, F64>(acc[RW - 1], pw1, iw1, ic[RW - 1], +1, p);
+                if (GHOST && has_dn) {
+                    float pw2[6], iw2[6];
+                    halo_window(hd[HROWS - 1], has_dn, has_left, has_right, lane, pw2);
+                    i_window(R + 1, iw2);
+                    relax_row<KIND, F64>(accG, pw1, iw1, ig, 0, p);
+                    relax_row<KIND, F64>(accG, pw2, iw2, ig, +1, p);
+                }
             }
         }
         // The previous plane's slot is no longer read by this warp.
@@ -600,14 +667,33 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
         // Border rows first: they are the neighbours' critical path.
         if (TOP) fin(0);
         if (BOT && (RW > 1 || !TOP)) fin(RW - 1);
-        if (j < J) publish_halo(j, Pout);
+        if (!TB || !A) {
+            if (TB && TOP) fin(1);
+            if (TB && BOT) fin(RW - 2);
+            if (j < J) publish_halo(j, Pout);
+        }
 #ifdef GD_SWEEP_TRACE
         if (TOP || BOT) trc[9] += clock64() - t_tail0_outer;
 #endif
-        if (GD_EARLY_POLL == 1 && j < J) early_poll(j);
 #pragma unroll
         for (int r = 0; r < RW; ++r)
             if (!((TOP && r == 0) || (BOT && r == RW - 1))) fin(r);
+        if (GHOST) {
+            const bool present = TOP ? has_up : has_dn;
+#pragma unroll
+            for (int q = 0; q < kC; ++q) {
+                G[q] = present ? accG[q].final(p) : INF;
+                if (!FULL && !colv[q]) G[q] = INF;
+            }
+            if (j < J) {
+                float* e = edge_own + (j & 1) * EPAR;
+                if (lane == 0) e[RW] = G[0];
+                if (lane == 31) e[ESL + RW] = G[kC - 1];
+            }
+            if (!backward && p.npass == 2 && present)
+                *reinterpret_cast<float4*>(gscr + static_cast<long long>(j >> 1) * VW) =
+                    make_float4(G[0], G[1], G[2], G[3]);
+        }
         if (j < J) publish_smem(j, Pout);
 
         // ---- store the relaxed plane ------------------------------------------
@@ -637,7 +723,6 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
         const bool near_turn = turn_fence && j <= n1 && j + NST >= n1;
         if (near_turn) fence_proxy_async_global();
 
-        if (GD_EARLY_POLL == 2 && j < J) early_poll(j);
         GD_T0(t_bar);
 #ifdef GD_SWEEP_TRACE
         if (TOP || BOT) trc[7] += t_bar - t_tail0_outer;
@@ -649,12 +734,14 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
         GD_TADD(10, t_post);
     };
 
+    const std::integral_constant<bool, true> kStepA{};
+    const std::integral_constant<bool, false> kStepB{};
     int j = 1;
     for (; j + 1 <= J; j += 2) {
-        step(j, PA, IA, PB, IB);
-        step(j + 1, PB, IB, PA, IA);
+        step(kStepA, j, PA, IA, PB, IB);
+        step(kStepB, j + 1, PB, IB, PA, IA);
     }
-    if (j <= J) step(j, PA, IA, PB, IB);
+    if (j <= J) step(kStepA, j, PA, IA, PB, IB);
 #ifdef GD_SWEEP_TRACE
     trc[4] = clock64() - t_begin;
     trc[5] = J;
@@ -669,14 +756,14 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p, const Ctx<RW
 // last warp is the TMA producer.  Slot j % NST carries plane p(j); it is
 // released ("empty") by every consumer warp during step j+1, which reads it as
 // the previous plane's intensities.
-template <int KIND, bool F64, int RW, int NWU, int NST, int MW>
+template <int KIND, bool F64, int RW, int NWU, int NST, int MW, bool TB>
 // One CTA per SM: two R = 2 CTAs per SM (126-register cap) measured 1.66 vs
 // 1.25 us/step for R = 4 at 512^3 -- twice the halo links cost more than the
 // second CTA hides (profiles/README.md).
 __global__ void __launch_bounds__((MW * NWU + 1) * 32, MW == 2 && NWU * RW == 4 ? GD_MINB2 : 1)
     sweep_kernel(const __grid_constant__ CUtensorMap tm_d, const __grid_constant__ CUtensorMap tm_i,
                  const __grid_constant__ SweepParams p) {
-    using L = Layout<RW, NWU, NST>;
+    using L = Layout<RW, NWU, NST, TB>;
     constexpr int DBOX = L::DBOX, IBOX = L::IBOX;
     constexpr bool kI = KIND != kSpatial;  // Spatial never reads intensities
     constexpr uint32_t TXW = static_cast<uint32_t>(kI ? DBOX * 4 + L::IBYTES : DBOX * 4);
@@ -686,12 +773,12 @@ __global__ void __launch_bounds__((MW * NWU + 1) * 32, MW == 2 && NWU * RW == 4 
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    Ctx<RW, NWU, NST> c;
+    Ctx<RW, NWU, NST, TB> c;
     c.sd = reinterpret_cast<float*>(smem_raw);
     c.si = c.sd + NST * nwv * DBOX;
     c.rows = c.si + NST * nwv * IBOX;
     c.edge = c.rows + 2 * NWU * 2 * nwv * kWV;
-    c.full = reinterpret_cast<uint64_t*>(c.edge + 2 * NWU * nwv * 2 * RW);
+    c.full = reinterpret_cast<uint64_t*>(c.edge + 2 * NWU * nwv * 2 * L::ESL);
     c.empty = c.full + NST;
     c.progress = reinterpret_cast<int*>(c.empty + NST);
     c.nwv = nwv;
@@ -733,12 +820,13 @@ __global__ void __launch_bounds__((MW * NWU + 1) * 32, MW == 2 && NWU * RW == 4 
                     float* dd = c.sd + (slot * nwv + cb) * DBOX;
                     float* di = c.si + (slot * nwv + cb) * IBOX;
                     const int v0 = cb * kWV;
+                    const int ud = c.u0 - L::DOFF, ui = c.u0 - L::IOFF;
                     if (p.tma_sweep_dim == 2) {
-                        tma_load_4d(dd, &tm_d, &c.full[slot], v0, c.u0, s, c.b);
-                        if (kI) tma_load_4d(di, &tm_i, &c.full[slot], v0 - 4, c.u0 - 1, s, c.b);
+                        tma_load_4d(dd, &tm_d, &c.full[slot], v0, ud, s, c.b);
+                        if (kI) tma_load_4d(di, &tm_i, &c.full[slot], v0 - 4, ui, s, c.b);
                     } else {
-                        tma_load_4d(dd, &tm_d, &c.full[slot], v0, s, c.u0, c.b);
-                        if (kI) tma_load_4d(di, &tm_i, &c.full[slot], v0 - 4, s, c.u0 - 1, c.b);
+                        tma_load_4d(dd, &tm_d, &c.full[slot], v0, s, ud, c.b);
+                        if (kI) tma_load_4d(di, &tm_i, &c.full[slot], v0 - 4, s, ui, c.b);
                     }
                 }
             }
@@ -759,9 +847,9 @@ __global__ void __launch_bounds__((MW * NWU + 1) * 32, MW == 2 && NWU * RW == 4 
 #define GD_ROLE(T, B)                                                                      \
     if (top == T && bot == B) {                                                            \
         if (full)                                                                          \
-            consumer_loop<KIND, F64, RW, NWU, NST, T, B, true>(p, c, wu, wv, lane);        \
+            consumer_loop<KIND, F64, RW, NWU, NST, TB, T, B, true>(p, c, wu, wv, lane);    \
         else                                                                               \
-            consumer_loop<KIND, F64, RW, NWU, NST, T, B, false>(p, c, wu, wv, lane);       \
+            consumer_loop<KIND, F64, RW, NWU, NST, TB, T, B, false>(p, c, wu, wv, lane);   \
         return;                                                                            \
     }
     if (NWU == 1) {
@@ -774,11 +862,11 @@ __global__ void __launch_bounds__((MW * NWU + 1) * 32, MW == 2 && NWU * RW == 4 
 #undef GD_ROLE
 }
 
-template <int KIND, bool F64, int RW, int NWU, int NST, int MW>
+template <int KIND, bool F64, int RW, int NWU, int NST, int MW, bool TB>
 cudaError_t launch_one(const CUtensorMap& tm_d, const CUtensorMap& tm_i, const SweepParams& p,
                        cudaStream_t stream) {
-    using L = Layout<RW, NWU, NST>;
-    auto fn = sweep_kernel<KIND, F64, RW, NWU, NST, MW>;
+    using L = Layout<RW, NWU, NST, TB>;
+    auto fn = sweep_kernel<KIND, F64, RW, NWU, NST, MW, TB>;
     const size_t smem = L::smem_bytes(p.nwv);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
@@ -791,10 +879,10 @@ cudaError_t launch_one(const CUtensorMap& tm_d, const CUtensorMap& tm_i, const S
                                        args, smem, stream);
 }
 
-template <int KIND, bool F64, int RW, int NWU, int NST, int MW>
+template <int KIND, bool F64, int RW, int NWU, int NST, int MW, bool TB>
 int coresident(int nwv) {
-    using L = Layout<RW, NWU, NST>;
-    auto fn = sweep_kernel<KIND, F64, RW, NWU, NST, MW>;
+    using L = Layout<RW, NWU, NST, TB>;
+    auto fn = sweep_kernel<KIND, F64, RW, NWU, NST, MW, TB>;
     const size_t smem = L::smem_bytes(nwv);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     int per_sm = 0;
@@ -813,30 +901,62 @@ int coresident(int nwv) {
 // flight per step; <= 512 columns run R = 4 as 2 warp rows of 2 rows (2 warps
 // per scheduler); R = 1 serves single-row planes (2D).  Wide planes (<= 2048
 // columns) trade registers for warps.
-#define GD_SWEEP_CASES(X)                                                          \
-    X(1, 1, 2, 6) X(2, 1, 2, 6) X(2, 2, 2, 6) X(4, 2, 2, 6) X(4, 4, 2, 4)             \
-    X(1, 1, 4, 6) X(2, 1, 4, 6) X(2, 2, 4, GD_NST4) X(4, 2, 4, 6)                     \
-    X(1, 1, 16, 6) X(2, 1, 16, 6) X(4, 1, 16, 6)
+#define GD_SWEEP_CASES(X)                                                                 \
+    X(1, 1, 2, 6, false) X(2, 1, 2, 6, false) X(2, 2, 2, 6, false) X(2, 2, 2, 6, true)      \
+    X(4, 2, 2, 6, false) X(4, 4, 2, 4, false) X(1, 4, 2, 6, false)                          \
+    X(1, 1, 4, 6, false) X(2, 1, 4, 6, false) X(2, 2, 4, GD_NST4, false)                    \
+    X(2, 2, 4, GD_NST4, true) X(4, 2, 4, 6, false) X(1, 4, 4, 6, false)                     \
+    X(1, 1, 16, 6, false) X(2, 1, 16, 6, false) X(4, 1, 16, 6, false)
 
 int width_class(int nwv) { return nwv <= 2 ? 2 : (nwv <= 4 ? 4 : 16); }
 
+// Rows-per-warp preference among shapes with the same R.  Blend runs R = 4 as
+// four warp rows of one row (16 consumer warps: its MUFU-heavy candidates need
+// the extra warps to hide latency; 23.1 vs 35.9 ms per 512^3 transform), the
+// min-plus kinds as two warp rows of two (fewer window builds per voxel; 13.3
+// vs 14.2 ms at lambda = 1).  -1: per-kind default; 0: the first listed.
+int g_sweep_rw = -1;
+int preferred_rw(int kind) { return g_sweep_rw >= 0 ? g_sweep_rw : (kind == kBlend ? 1 : 0); }
+// The preferred shape exists for (R, width class, tb)?
+bool rw_pref_exists(int R, int mw, bool tb, int rw) {
+#define GD_CASE(RWW, NW, MM, NS, T) \
+    if (R == RWW * NW && mw == MM && tb == T && RWW == rw) return true;
+    GD_SWEEP_CASES(GD_CASE)
+#undef GD_CASE
+    return false;
+}
+// Shape filter: the preferred rows-per-warp when it exists, else the first listed.
+struct RwSel {
+    int want;
+    RwSel(int R, int mw, bool tb, int rw) : want(rw_pref_exists(R, mw, tb, rw) ? rw : 0) {}
+    bool ok(int rww) { return want == 0 ? take_first() : rww == want; }
+    bool first = true;
+    bool take_first() {
+        const bool f = first;
+        first = false;
+        return f;
+    }
+};
+
 template <int KIND, bool F64>
-cudaError_t dispatch_r(int R, const CUtensorMap& tm_d, const CUtensorMap& tm_i,
+cudaError_t dispatch_r(int R, bool tb, const CUtensorMap& tm_d, const CUtensorMap& tm_i,
                        const SweepParams& p, cudaStream_t s) {
     const int mw = width_class(p.nwv);
-#define GD_CASE(RWW, NW, MM, NS)                                     \
-    if (R == RWW * NW && mw == MM)                                   \
-        return launch_one<KIND, F64, RWW, NW, NS, MM>(tm_d, tm_i, p, s);
+    RwSel sel(R, mw, tb, preferred_rw(KIND));
+#define GD_CASE(RWW, NW, MM, NS, T)                                  \
+    if (R == RWW * NW && mw == MM && tb == T && sel.ok(RWW))         \
+        return launch_one<KIND, F64, RWW, NW, NS, MM, T>(tm_d, tm_i, p, s);
     GD_SWEEP_CASES(GD_CASE)
 #undef GD_CASE
     return cudaErrorInvalidValue;
 }
 
 template <int KIND, bool F64>
-int dispatch_cores(int R, int nwv) {
+int dispatch_cores(int R, bool tb, int nwv) {
     const int mw = width_class(nwv);
-#define GD_CASE(RWW, NW, MM, NS) \
-    if (R == RWW * NW && mw == MM) return coresident<KIND, F64, RWW, NW, NS, MM>(nwv);
+    RwSel sel(R, mw, tb, preferred_rw(KIND));
+#define GD_CASE(RWW, NW, MM, NS, T) \
+    if (R == RWW * NW && mw == MM && tb == T && sel.ok(RWW)) return coresident<KIND, F64, RWW, NW, NS, MM, T>(nwv);
     GD_SWEEP_CASES(GD_CASE)
 #undef GD_CASE
     return 0;
@@ -844,38 +964,51 @@ int dispatch_cores(int R, int nwv) {
 
 }  // namespace
 
-cudaError_t launch_sweep(int kind, bool f64, int R, const CUtensorMap& tm_d,
+cudaError_t launch_sweep(int kind, bool f64, int R, bool tb, const CUtensorMap& tm_d,
                          const CUtensorMap& tm_i, const SweepParams& p, cudaStream_t stream) {
     switch (kind) {
         case kSpatial:
-            return dispatch_r<kSpatial, false>(R, tm_d, tm_i, p, stream);
+            return dispatch_r<kSpatial, false>(R, tb, tm_d, tm_i, p, stream);
         case kIntensity:
-            return f64 ? dispatch_r<kIntensity, true>(R, tm_d, tm_i, p, stream)
-                       : dispatch_r<kIntensity, false>(R, tm_d, tm_i, p, stream);
+            return f64 ? dispatch_r<kIntensity, true>(R, tb, tm_d, tm_i, p, stream)
+                       : dispatch_r<kIntensity, false>(R, tb, tm_d, tm_i, p, stream);
         default:
-            return f64 ? dispatch_r<kBlend, true>(R, tm_d, tm_i, p, stream)
-                       : dispatch_r<kBlend, false>(R, tm_d, tm_i, p, stream);
+            return f64 ? dispatch_r<kBlend, true>(R, tb, tm_d, tm_i, p, stream)
+                       : dispatch_r<kBlend, false>(R, tb, tm_d, tm_i, p, stream);
     }
 }
 
-int sweep_warp_rows(int R, int nwv) {
+void sweep_set_rows_per_warp(int rw) { g_sweep_rw = rw; }
+
+int sweep_warp_rows(int R, int nwv, int kind) {
     const int mw = width_class(nwv);
-#define GD_CASE(RWW, NW, MM, NS) \
-    if (R == RWW * NW && mw == MM) return NW;
+    RwSel sel(R, mw, false, preferred_rw(kind));
+#define GD_CASE(RWW, NW, MM, NS, T) \
+    if (R == RWW * NW && mw == MM && !T && sel.ok(RWW)) return NW;
     GD_SWEEP_CASES(GD_CASE)
 #undef GD_CASE
     return 0;
 }
 
-int sweep_max_coresident(int R, int nwv, int kind, bool f64) {
+bool sweep_has_tb(int R, int nwv, int kind) {
+    const int mw = width_class(nwv);
+    RwSel sel(R, mw, true, preferred_rw(kind));
+#define GD_CASE(RWW, NW, MM, NS, T) \
+    if (R == RWW * NW && mw == MM && T && sel.ok(RWW)) return true;
+    GD_SWEEP_CASES(GD_CASE)
+#undef GD_CASE
+    return false;
+}
+
+int sweep_max_coresident(int R, bool tb, int nwv, int kind, bool f64) {
     switch (kind) {
-        case kSpatial: return dispatch_cores<kSpatial, false>(R, nwv);
+        case kSpatial: return dispatch_cores<kSpatial, false>(R, tb, nwv);
         case kIntensity:
-            return f64 ? dispatch_cores<kIntensity, true>(R, nwv)
-                       : dispatch_cores<kIntensity, false>(R, nwv);
+            return f64 ? dispatch_cores<kIntensity, true>(R, tb, nwv)
+                       : dispatch_cores<kIntensity, false>(R, tb, nwv);
         default:
-            return f64 ? dispatch_cores<kBlend, true>(R, nwv)
-                       : dispatch_cores<kBlend, false>(R, nwv);
+            return f64 ? dispatch_cores<kBlend, true>(R, tb, nwv)
+                       : dispatch_cores<kBlend, false>(R, tb, nwv);
     }
 }
 

@@ -74,6 +74,7 @@ struct SweepParams {
     uint32_t tag_base;
     unsigned long long* halo; // tagged halo words: [strip][parity][TOP|BOT][nwv*128]
     long long* trace;         // optional per-warp cycle counters (null in production)
+    float* ghost;             // TB: forward ghost rows, [cta][TOP|BOT][n1/2+1][nwv*128]
     int debug_flags;          // experiments only (GD_SWEEP_TRACE builds): 1 no spin, 2 no halo stores, 4 no halo loads
     // Neighbour coefficients indexed (du+1)*3 + (dv+1).
     double rho[9];
@@ -83,11 +84,18 @@ struct SweepParams {
     float lambda_f;
 };
 
-// Host-side launch (defined in sweep.cu).  R = rows per strip.
-cudaError_t launch_sweep(int kind, bool f64, int R, const CUtensorMap& tm_d,
+// Host-side launch (defined in sweep.cu).  R = rows per strip; tb = the
+// temporally blocked variant (halo every two planes; boxes with ghost rows:
+// distances R + 2 rows from u0 - 1, intensities R + 4 rows from u0 - 2; halo
+// 2 rows per side).
+cudaError_t launch_sweep(int kind, bool f64, int R, bool tb, const CUtensorMap& tm_d,
                          const CUtensorMap& tm_i, const SweepParams& p, cudaStream_t stream);
 // Warp rows (NWU) of the strip shape serving R rows at this width; 0 = none.
-int sweep_warp_rows(int R, int nwv);
-int sweep_max_coresident(int R, int nwv, int kind, bool f64);
+int sweep_warp_rows(int R, int nwv, int kind);
+// Experiments: prefer strip shapes with this many rows per warp (-1 = per-kind default).
+void sweep_set_rows_per_warp(int rw);
+// Whether a temporally blocked variant exists for this strip shape.
+bool sweep_has_tb(int R, int nwv, int kind);
+int sweep_max_coresident(int R, bool tb, int nwv, int kind, bool f64);
 
 }  // namespace gdb

@@ -1,0 +1,23 @@
+"""Kernel variants reachable only through tuning switches (read once per process),
+checked in a subprocess against the C oracle: temporal blocking over plane pairs
+(GEODIST_SWEEP_TB=1), the one-row-per-warp strip shape for every cost kind
+(GEODIST_SWEEP_RW=1) and the two-rows-per-warp shape for blend (RW=2)."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.mark.parametrize("env", [{"GEODIST_SWEEP_TB": "1"}, {"GEODIST_SWEEP_RW": "1"},
+                                 {"GEODIST_SWEEP_RW": "2"}],
+                         ids=["tb", "rw1", "rw2"])
+def test_variant_parity(env):
+    e = dict(os.environ, **env)
+    r = subprocess.run([sys.executable, os.path.join(HERE, "_variant_check.py")], env=e,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
