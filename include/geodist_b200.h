@@ -34,7 +34,8 @@ enum gd_status {
     GD_INVALID_ARGUMENT = 1, /* reference: std::invalid_argument */
     GD_EMPTY_SEEDS = 2,      /* reference: geodist::EmptySeedsError (transforms.hpp:11-14) */
     GD_CUDA_ERROR = 3,       /* device failure; C++ layer throws std::runtime_error */
-    GD_UNSUPPORTED = 4       /* shape beyond the kernels' co-residency limit */
+    GD_UNSUPPORTED = 4       /* reserved: every shape runs (planes beyond the persistent kernel's
+                                co-residency or width limit take the plane-step fallback) */
 };
 
 enum gd_mem { GD_MEM_HOST = 0, GD_MEM_DEVICE = 1 };

@@ -280,9 +280,8 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
     const int kind = cost_kind(lambda);
     if (kind == kSpatial) ibase = dbase;  // intensities never read; any valid map will do
     const int nwv = (nv + kWV - 1) / kWV;
-    if (nwv > kMaxWarps)
-        return {kUnsupported, "plane width " + std::to_string(nv) + " exceeds " +
-                                  std::to_string(kMaxWarps * kWV) + " columns"};
+    static const bool force_fallback =
+        std::getenv("GEODIST_SWEEP_FALLBACK") && std::atoi(std::getenv("GEODIST_SWEEP_FALLBACK")) == 1;
     // Rows per strip.  Every strip of a volume must be co-resident (the halo
     // chain spins); volumes beyond what fits run in sequential launch groups.
     // Cost = groups x relative per-step cost of the strip shape (taller strips
@@ -309,6 +308,7 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
     bool tb = false;
     double best = 0.0;
     for (int cand : {4, 8, 16, 2, 1}) {
+        if (nwv > kMaxWarps || force_fallback) break;
         if ((nu == 1) != (cand == 1)) continue;
         if (sweep_warp_rows(cand, nwv, kind) == 0) continue;
         const bool tbc = tb_env && sweep_has_tb(cand, nwv, kind) && nu > cand;
@@ -328,11 +328,10 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
             tb = tbc;
         }
     }
-    if (R == 0)
-        return {kUnsupported, "plane of " + std::to_string(nu) + "x" + std::to_string(nv) +
-                                  " has more row strips than co-resident CTAs"};
+    // R == 0: the plane is wider than kMaxWarps * 128 columns or has more row
+    // strips than co-resident CTAs -> the plane-step fallback below.
     const int ntu = static_cast<int>(per_vol);
-    const int group = static_cast<int>(std::min<long long>(w.B, maxc / per_vol));
+    const int group = R ? static_cast<int>(std::min<long long>(w.B, maxc / per_vol)) : 0;
     const int hrows = tb ? 2 : 1, doff = tb ? 1 : 0, ioff = tb ? 2 : 1;
     const long long strip_words = 2ll * 2 * hrows * nwv * kWV;
     const int J = npass * (ns - 1);
@@ -358,6 +357,28 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
             p.c0[k] = blend_c0(lambda, rho);
             p.c0_f[k] = static_cast<float>(p.c0[k]);
         }
+
+    if (R == 0) {
+        // One launch per plane step (plane_step_kernel), every volume at once.
+        const int n1 = ns - 1;
+        auto plane = [&](int j) {
+            if (j <= n1) return first_orient > 0 ? j : n1 - j;
+            const int k = j - n1;
+            return first_orient > 0 ? n1 - k : k;
+        };
+        for (int b0 = 0; b0 < w.B; b0 += 65535) {
+            p.nvol = std::min(65535, w.B - b0);
+            p.dist = dbase + b0 * vol;
+            p.image = ibase + b0 * vol;
+            const double bytes = static_cast<double>(p.nvol) * g.voxels() * npass *
+                                 (kind == kSpatial ? 8.0 : 12.0);
+            ProfScope ps(kProfSweep, bytes, s);
+            for (int j = 1; j <= J; ++j) GD_CK(launch_plane_step(kind, f64, p, plane(j), plane(j - 1), s));
+            g_launches += J;
+            if (st) st->kernel_launches += J;
+        }
+        return Status::Ok();
+    }
 
     uint32_t box_d[4], box_i[4];
     const uint32_t drows = R + 2 * doff, irows = R + 2 * ioff;

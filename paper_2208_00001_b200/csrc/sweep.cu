@@ -752,6 +752,64 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p,
 #endif
 }
 
+// Plane-step fallback (any plane size): one thread relaxes 4 consecutive
+// columns of one row of plane s from plane sp, reading the previous plane from
+// global memory (L2-resident: it was written by the previous launch).  Same
+// arithmetic as the persistent kernel (relax_row / Acc), so results agree bit
+// for bit.  Columns >= nv of a padded row are never read as neighbours nor written.
+template <int KIND, bool F64>
+__global__ void __launch_bounds__(256)
+    plane_step_kernel(const __grid_constant__ SweepParams p, int s, int sp) {
+    constexpr bool kI = KIND != kSpatial;
+    const int nq = (p.nv + kC - 1) / kC;
+    const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= static_cast<long long>(p.nu) * nq) return;
+    const int u = static_cast<int>(idx / nq), v0 = static_cast<int>(idx % nq) * kC;
+    const long long vb = static_cast<long long>(blockIdx.y) * p.vol_stride;
+    const float INF = finf();
+    const float* dprev = p.dist + vb + static_cast<long long>(sp) * p.ss;
+    float* dcur = p.dist + vb + static_cast<long long>(s) * p.ss + static_cast<long long>(u) * p.su;
+    const float* iprev = p.image + vb + static_cast<long long>(sp) * p.ss;
+    const float* icur = p.image + vb + static_cast<long long>(s) * p.ss +
+                        static_cast<long long>(u) * p.su;
+    float ip[kC];
+    Acc<KIND, F64> acc[kC];
+#pragma unroll
+    for (int q = 0; q < kC; ++q) {
+        const bool ok = v0 + q < p.nv;
+        acc[q].init(ok ? dcur[v0 + q] : INF);
+        ip[q] = (kI && ok) ? icur[v0 + q] : 0.0f;
+    }
+#pragma unroll
+    for (int du = -1; du <= 1; ++du) {
+        const int uu = u + du;
+        if (uu < 0 || uu >= p.nu) continue;
+        const float* dr = dprev + static_cast<long long>(uu) * p.su;
+        const float* ir = iprev + static_cast<long long>(uu) * p.su;
+        float pw[6], iw[6];
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+            const int v = v0 - 1 + i;
+            const bool ok = v >= 0 && v < p.nv;
+            pw[i] = ok ? dr[v] : INF;
+            iw[i] = (kI && ok) ? ir[v] : 0.0f;
+        }
+        // relax_row's du is (previous-plane row) - (output row), as here
+        relax_row<KIND, F64>(acc, pw, iw, ip, du, p);
+    }
+#pragma unroll
+    for (int q = 0; q < kC; ++q)
+        if (v0 + q < p.nv) dcur[v0 + q] = acc[q].final(p);
+}
+
+template <int KIND, bool F64>
+cudaError_t plane_step_one(const SweepParams& p, int s, int sp, cudaStream_t stream) {
+    const long long n = static_cast<long long>(p.nu) * ((p.nv + kC - 1) / kC);
+    const dim3 grid(static_cast<unsigned>((n + 255) / 256), static_cast<unsigned>(p.nvol));
+    plane_step_kernel<KIND, F64><<<grid, 256, 0, stream>>>(p, s, sp);
+    return cudaGetLastError();
+}
+
 // Warp-specialised persistent sweep: warps [0, NWU*nwv) relax the strip, the
 // last warp is the TMA producer.  Slot j % NST carries plane p(j); it is
 // released ("empty") by every consumer warp during step j+1, which reads it as
@@ -884,11 +942,17 @@ int coresident(int nwv) {
     using L = Layout<RW, NWU, NST, TB>;
     auto fn = sweep_kernel<KIND, F64, RW, NWU, NST, MW, TB>;
     const size_t smem = L::smem_bytes(nwv);
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem)) != cudaSuccess) {
+        (void)cudaGetLastError();  // too much shared memory at this width: not a candidate
+        return 0;
+    }
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, (nwv * NWU + 1) * 32, smem) !=
-        cudaSuccess)
+        cudaSuccess) {
+        (void)cudaGetLastError();
         return 0;
+    }
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -975,6 +1039,19 @@ cudaError_t launch_sweep(int kind, bool f64, int R, bool tb, const CUtensorMap& 
         default:
             return f64 ? dispatch_r<kBlend, true>(R, tb, tm_d, tm_i, p, stream)
                        : dispatch_r<kBlend, false>(R, tb, tm_d, tm_i, p, stream);
+    }
+}
+
+cudaError_t launch_plane_step(int kind, bool f64, const SweepParams& p, int s, int sp,
+                              cudaStream_t stream) {
+    switch (kind) {
+        case kSpatial: return plane_step_one<kSpatial, false>(p, s, sp, stream);
+        case kIntensity:
+            return f64 ? plane_step_one<kIntensity, true>(p, s, sp, stream)
+                       : plane_step_one<kIntensity, false>(p, s, sp, stream);
+        default:
+            return f64 ? plane_step_one<kBlend, true>(p, s, sp, stream)
+                       : plane_step_one<kBlend, false>(p, s, sp, stream);
     }
 }
 

@@ -39,7 +39,7 @@
 //   * Intensity (lambda == 1): f32 `d_q + |I_p - I_q|` is exactly the
 //     reference's f32(f64(d_q) + |di|) whenever I_p - I_q is exact in f32; the
 //     host checks that per image (image_check_kernel) and otherwise selects the
-//     f64 path.  Column pairs go through packed FADD2 (sm_100 f32x2).
+//     f64 path.
 //   * Blend: f32 arithmetic within the 1e-6 abs + 1e-5 rel tolerance; the f64
 //     path (sqrt(fma(lambda*di, di, c0)) exactly as compiled in the reference)
 //     when exact mode is requested.
@@ -75,6 +75,7 @@ struct SweepParams {
     unsigned long long* halo; // tagged halo words: [strip][parity][TOP|BOT][nwv*128]
     long long* trace;         // optional per-warp cycle counters (null in production)
     float* ghost;             // TB: forward ghost rows, [cta][TOP|BOT][n1/2+1][nwv*128]
+    const float* image;       // plane-step fallback: intensities (same layout as dist)
     int debug_flags;          // experiments only (GD_SWEEP_TRACE builds): 1 no spin, 2 no halo stores, 4 no halo loads
     // Neighbour coefficients indexed (du+1)*3 + (dv+1).
     double rho[9];
@@ -92,6 +93,11 @@ cudaError_t launch_sweep(int kind, bool f64, int R, bool tb, const CUtensorMap& 
                          const CUtensorMap& tm_i, const SweepParams& p, cudaStream_t stream);
 // Warp rows (NWU) of the strip shape serving R rows at this width; 0 = none.
 int sweep_warp_rows(int R, int nwv, int kind);
+// Fallback for planes the persistent kernel cannot hold co-resident (more row
+// strips than CTAs, or wider than kMaxWarps * 128 columns): one launch per
+// plane step, plane s relaxed from plane sp, all `p.nvol` volumes at once.
+cudaError_t launch_plane_step(int kind, bool f64, const SweepParams& p, int s, int sp,
+                              cudaStream_t stream);
 // Experiments: prefer strip shapes with this many rows per warp (-1 = per-kind default).
 void sweep_set_rows_per_warp(int rw);
 // Whether a temporally blocked variant exists for this strip shape.

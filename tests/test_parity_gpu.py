@@ -129,6 +129,20 @@ def test_batched_tall_strips(gd, oracle, lam, shape):
         _check(g[b], r, lam)
 
 
+@pytest.mark.parametrize("shape", [(3, 6, 2100), (3, 1300, 600)],
+                         ids=["wider_than_2048", "more_strips_than_sms"])
+def test_large_planes_plane_step(gd, oracle, shape):
+    """Planes the persistent kernel cannot hold (W > 2048 columns; 325 strips of
+    4 rows > the co-resident CTAs) run the one-launch-per-plane fallback."""
+    rng = np.random.default_rng(29)
+    img = dyadic_image(rng, shape)
+    mask = point_mask(shape)
+    for lam in (0.0, 1.0):
+        g = gd.generalized_geodesic(img, mask, (1.0, 1.0, 1.0), lam, 1e10, 1)
+        r = oracle.generalized_geodesic(img, mask, (1.0, 1.0, 1.0), lam, 1e10, 1)
+        assert bitwise_equal(g, r), parity(g, r)
+
+
 @pytest.mark.parametrize("lam", [0.0, 1.0])
 def test_gsf(gd, oracle, lam):
     shape = (24, 32, 28)

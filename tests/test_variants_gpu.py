@@ -1,7 +1,8 @@
 """Kernel variants reachable only through tuning switches (read once per process),
 checked in a subprocess against the C oracle: temporal blocking over plane pairs
 (GEODIST_SWEEP_TB=1), the one-row-per-warp strip shape for every cost kind
-(GEODIST_SWEEP_RW=1) and the two-rows-per-warp shape for blend (RW=2)."""
+(GEODIST_SWEEP_RW=1), the two-rows-per-warp shape for blend (RW=2) and the
+plane-step fallback for every plane (GEODIST_SWEEP_FALLBACK=1)."""
 import os
 import subprocess
 import sys
@@ -14,8 +15,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 @pytest.mark.parametrize("env", [{"GEODIST_SWEEP_TB": "1"}, {"GEODIST_SWEEP_RW": "1"},
-                                 {"GEODIST_SWEEP_RW": "2"}],
-                         ids=["tb", "rw1", "rw2"])
+                                 {"GEODIST_SWEEP_RW": "2"}, {"GEODIST_SWEEP_FALLBACK": "1"}],
+                         ids=["tb", "rw1", "rw2", "plane_step"])
 def test_variant_parity(env):
     e = dict(os.environ, **env)
     r = subprocess.run([sys.executable, os.path.join(HERE, "_variant_check.py")], env=e,
