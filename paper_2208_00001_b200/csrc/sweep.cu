@@ -35,9 +35,12 @@ __device__ __forceinline__ float2 f2_add(float2 a, float2 b) {
     return bits_f2(r);
 }
 
+// MUFU.SQRT alone: .ftz drops the denormal-range rescaling (FSETP + 2 FMUL per
+// candidate).  x = lambda di^2 + c0 is denormal only when both terms are below
+// 1.2e-38, far inside the 1e-6 absolute tolerance.
 __device__ __forceinline__ float sqrt_approx(float x) {
     float r;
-    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
 }
 
@@ -737,6 +740,8 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p,
     const std::integral_constant<bool, true> kStepA{};
     const std::integral_constant<bool, false> kStepB{};
     int j = 1;
+    // (A single step body with register moves instead of the unrolled pair
+    // measured slower for the one-row shape: 19.5 vs 18.0 ms at lambda = 0.5.)
     for (; j + 1 <= J; j += 2) {
         step(kStepA, j, PA, IA, PB, IB);
         step(kStepB, j + 1, PB, IB, PA, IA);

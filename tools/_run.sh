@@ -1,1 +1,2 @@
-for rw in -1 4; do echo "== RW=$rw"; GEODIST_SWEEP_RW=$rw timeout 200 python tools/time_configs.py --only batch64_256; GEODIST_SWEEP_RW=$rw timeout 200 python tools/time_configs.py --only gsf; done > gpurun_out/rw4.txt 2>&1
+timeout 200 python tools/time_configs.py --only 3d_512 > gpurun_out/ftz2.txt 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2 >> gpurun_out/ftz2.txt
