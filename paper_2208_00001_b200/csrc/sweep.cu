@@ -569,7 +569,7 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p,
             const float4 q4 = *reinterpret_cast<const float4*>(rp + vl);
             const float c4[kC] = {q4.x, q4.y, q4.z, q4.w};
             float pw[6], iw[6];
-            make_window(c4, has_left ? rp[vl - 1] : INF, has_right ? rp[vl + kC] : INF, lane, pw);
+            make_window(c4, edge_l ? rp[vl - 1] : INF, edge_r ? rp[vl + kC] : INF, lane, pw);
             i_window(r0 - 1, iw);
             relax_row<KIND, F64>(acc[0], pw, iw, ic[0], -1, p);
         }
@@ -578,7 +578,7 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p,
             const float4 q4 = *reinterpret_cast<const float4*>(rp + vl);
             const float c4[kC] = {q4.x, q4.y, q4.z, q4.w};
             float pw[6], iw[6];
-            make_window(c4, has_left ? rp[vl - 1] : INF, has_right ? rp[vl + kC] : INF, lane, pw);
+            make_window(c4, edge_l ? rp[vl - 1] : INF, edge_r ? rp[vl + kC] : INF, lane, pw);
             i_window(r0 + RW, iw);
             relax_row<KIND, F64>(acc[RW - 1], pw, iw, ic[RW - 1], +1, p);
         }
