@@ -12,7 +12,7 @@
 #include "engine.cuh"
 
 namespace gdb {
-int sweep_max_coresident(int R, bool tb, int nwv, int kind, bool f64);  // sweep.cu
+int sweep_max_coresident(int R, bool tb, int nwv, int kind, bool f64, int cs);  // sweep.cu
 }
 
 namespace {
@@ -234,5 +234,5 @@ int gd_fill_splitmix(float* device_out, long long n, unsigned long long seed, vo
 
 // Diagnostics: co-resident CTA capacity of one sweep configuration.
 extern "C" int gd_debug_coresident(int R, int nwv, int kind, int f64) {
-    return gdb::sweep_max_coresident(R, false, nwv, kind, f64 != 0);
+    return gdb::sweep_max_coresident(R, false, nwv, kind, f64 != 0, 1);
 }

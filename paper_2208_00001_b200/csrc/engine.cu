@@ -332,6 +332,29 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
     // strips than co-resident CTAs -> the plane-step fallback below.
     const int ntu = static_cast<int>(per_vol);
     const int group = R ? static_cast<int>(std::min<long long>(w.B, maxc / per_vol)) : 0;
+    // Thread-block clusters for the halo (GEODIST_SWEEP_CLUSTER=<cs>): strips of one
+    // cluster exchange rows through DSMEM.  Needs the launch group to tile into
+    // co-resident clusters; otherwise every link uses the tagged L2 words.
+    // Default (measured on B200): clusters of 4 (else 2) for the intensity kind on
+    // wide planes with many strips -- 512^3 lambda=1: 11.8 vs 13.5 ms of sweep, the
+    // fewer L2 halo words shortening the remaining L2 links' round trip.  Blend
+    // (16-warp shape), small planes and batches measured slower clustered; clusters
+    // of 8 / 16 do not tile 128 CTAs co-resident.
+    static const int cs_env =
+        std::getenv("GEODIST_SWEEP_CLUSTER") ? std::atoi(std::getenv("GEODIST_SWEEP_CLUSTER")) : -1;
+    int cs = 1;
+    const bool cs_default = kind == kIntensity && nwv >= 4 && ntu >= 64;
+    if (R && !tb && ntu > 1 && (cs_env >= 0 || cs_default) && sweep_has_cluster(R, nwv, kind)) {
+        const long long ctas = static_cast<long long>(group) * ntu;
+        const int tries[3] = {cs_env >= 0 ? cs_env : 4, cs_env >= 0 ? 0 : 2, 0};
+        for (int cand : tries) {
+            if (cand < 2 || cand > 16) continue;
+            if (ctas % cand == 0 && sweep_max_coresident(R, false, nwv, kind, f64, cand) >= ctas) {
+                cs = cand;
+                break;
+            }
+        }
+    }
     const int hrows = tb ? 2 : 1, doff = tb ? 1 : 0, ioff = tb ? 2 : 1;
     const long long strip_words = 2ll * 2 * hrows * nwv * kWV;
     const int J = npass * (ns - 1);
@@ -343,6 +366,7 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
     p.first_orient = first_orient;
     p.npass = npass;
     p.fence_turn = npass == 2 ? 1 : 0;
+    p.cs = cs;
     p.lambda = lambda;
     p.lambda_f = static_cast<float>(lambda);
     for (int du = -1; du <= 1; ++du)
@@ -409,6 +433,7 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
         }
         p.dist = dbase + b0 * vol;
         p.nvol = nvol;
+        p.cs = (static_cast<long long>(nvol) * ntu) % cs == 0 ? cs : 1;  // last group may be short
         p.halo = sc.halo.as<unsigned long long>();
         p.ghost = nullptr;
         if (tb && npass == 2) {

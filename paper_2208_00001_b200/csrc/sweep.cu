@@ -186,11 +186,14 @@ struct Layout {
     static constexpr int DBOX = (R + 2 * DOFF) * kWV;             // floats per column-block box
     static constexpr int IBOX = ((R + 2 * IOFF) * kIW + 31) / 32 * 32;  // 128-B aligned stride
     static constexpr int IBYTES = (R + 2 * IOFF) * kIW * 4;
-    static size_t smem_bytes(int nwv) {
+    // ds: DSMEM receive rows for cluster links (only allocated when clustered:
+    // 2 KB more per CTA cost narrow planes their third CTA per SM).
+    static size_t smem_bytes(int nwv, bool ds = false) {
         return static_cast<size_t>(NST) * nwv * (DBOX + IBOX) * 4     // TMA ring
                + static_cast<size_t>(2) * NWU * 2 * nwv * kWV * 4     // warp-row boundary rows
                + static_cast<size_t>(2) * NWU * nwv * 2 * ESL * 4     // warp-edge columns
-               + 2 * NST * 8 + 16 + 128;                              // barriers, progress
+               + (ds ? static_cast<size_t>(2) * 2 * nwv * kWV * 4 : 0)  // DSMEM halo rows
+               + 2 * NST * 8 + 4 * 8 + 16 + 128;                      // barriers, progress
     }
 };
 
@@ -257,10 +260,12 @@ struct Ctx {
     float* si;          // [NST][nwv][R+2][136]    intensities + row halo (TMA)
     float* rows;        // [2][NWU][first|last][nwv*128] warp-row boundary rows
     float* edge;        // [2][NWU][nwv][left|right][RW] warp-edge columns
+    float* recv;        // [2 parities][above|below][nwv*128] DSMEM halo rows (cluster links)
     uint64_t* full;     // [NST]
     uint64_t* empty;    // [NST]
+    uint64_t* rbar;     // [2 parities][above|below]: complete_tx of the DSMEM rows
     int* progress;
-    int nwv, g, b, tu, u0, n1, J, VW;
+    int nwv, g, b, tu, u0, n1, J, VW, rank;
 };
 
 template <int RW, int NWU, int NST, bool TB>
@@ -274,7 +279,8 @@ __device__ __forceinline__ int plane_of(const SweepParams& p, const Ctx<RW, NWU,
 // One consumer warp's whole sweep.  TOP / BOT: the warp row borders the strip
 // above / below (tagged global halo); FULL: every voxel of the warp is inside
 // the volume.  Specialising on the role keeps the per-step body branch-free.
-template <int KIND, bool F64, int RW, int NWU, int NST, bool TB, bool TOP, bool BOT, bool FULL>
+template <int KIND, bool F64, int RW, int NWU, int NST, bool TB, bool CL, bool TOP, bool BOT,
+          bool FULL>
 __device__ __forceinline__ void consumer_loop(const SweepParams& p,
                                               const Ctx<RW, NWU, NST, TB>& c, int wu, int wv,
                                               int lane) {
@@ -312,6 +318,14 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p,
     const unsigned long long* dn0 = p.halo + (strip0 + c.tu + 1) * strip_words + hl;
     unsigned long long* self0 = p.halo + static_cast<long long>(c.g) * strip_words + hl;
     const bool pub_up = TOP && c.tu > 0, pub_dn = BOT && c.tu + 1 < p.ntu;
+    // Links inside a thread-block cluster (consecutive strips of one volume)
+    // carry the row through DSMEM: st.async into the neighbour's receive row,
+    // completing tx bytes on its mbarrier; links across clusters use the tagged
+    // L2 words.  (Not combined with temporal blocking.)
+    const int rank = c.rank;
+    const bool ds_up = CL && has_up && rank > 0;
+    const bool ds_dn = CL && has_dn && rank + 1 < p.cs;
+    const bool l2_up = has_up && !ds_up, l2_dn = has_dn && !ds_dn;
     // neighbour-warp edge columns (ESL slots per side: own rows, then the ghost row)
     const int eoffL = ((wu * nwv + wv - 1) * 2 + 1) * ESL;
     const int eoffR = ((wu * nwv + wv + 1) * 2 + 0) * ESL;
@@ -352,14 +366,24 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p,
         const uint32_t tag = tag_base + static_cast<uint32_t>(j);
         unsigned long long* q = self0 + par * PARW;
         if (GD_DBG(2)) return;
-        if (pub_up) {
+        if (ds_up || ds_dn) {
+            // to the neighbour above: its "below" row; to the one below: its "above" row
+            const int side = ds_up ? 1 : 0;
+            const int r = ds_up ? 0 : RW - 1;
+            const uint32_t dst = static_cast<uint32_t>(rank + (ds_up ? -1 : 1));
+            const uint32_t raddr =
+                mapa_shared(smem_u32(c.recv + (par * 2 + side) * VW + vl), dst);
+            const uint32_t rbar = mapa_shared(smem_u32(&c.rbar[par * 2 + side]), dst);
+            st_async_v4(raddr, N[r][0], N[r][1], N[r][2], N[r][3], rbar);
+        }
+        if (pub_up && !ds_up) {
 #pragma unroll
             for (int k = 0; k < HROWS; ++k) {
                 st_tagged2(q + k * VW, N[k][0], N[k][1], tag);
                 st_tagged2(q + k * VW + 64, N[k][2], N[k][3], tag);
             }
         }
-        if (pub_dn) {
+        if (pub_dn && !ds_dn) {
 #pragma unroll
             for (int k = 0; k < HROWS; ++k) {
                 const int r = RW - HROWS + k;
@@ -469,9 +493,16 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p,
         if (POLL && !GD_DBG(4)) {
 #pragma unroll
             for (int k = 0; k < HROWS; ++k) {
-                if (TOP && has_up) load_row(hup + k * VW, hu[k]);
-                if (BOT && has_dn) load_row(hdn + k * VW, hd[k]);
+                if (TOP && l2_up) load_row(hup + k * VW, hu[k]);
+                if (BOT && l2_dn) load_row(hdn + k * VW, hd[k]);
             }
+        }
+        // DSMEM rows of step j-1: one thread per receiving warp row arms the
+        // mbarrier phase with the row's bytes (the data may already be there).
+        const int rq = (j - 1) & 1;
+        if (POLL && wv == 0 && lane == 0) {
+            if (ds_up) mbar_arrive_expect_tx(&c.rbar[rq * 2 + 0], static_cast<uint32_t>(VW * 4));
+            if (ds_dn) mbar_arrive_expect_tx(&c.rbar[rq * 2 + 1], static_cast<uint32_t>(VW * 4));
         }
         const bool backward = j > n1;
         const int gslot = (2 * n1 - j) >> 1;  // backward A step: forward step 2 n1 - j
@@ -610,26 +641,39 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p,
                 bool ok = true;
 #pragma unroll
                 for (int k = 0; k < HROWS; ++k) {
-                    if (TOP && has_up) ok = ok && fresh(hu[k]);
-                    if (BOT && has_dn) ok = ok && fresh(hd[k]);
+                    if (TOP && l2_up) ok = ok && fresh(hu[k]);
+                    if (BOT && l2_dn) ok = ok && fresh(hd[k]);
                 }
                 if (__all_sync(kFull, ok)) break;
 #pragma unroll
                 for (int k = 0; k < HROWS; ++k) {
-                    if (TOP && has_up) load_row(hup + k * VW, hu[k]);
-                    if (BOT && has_dn) load_row(hdn + k * VW, hd[k]);
+                    if (TOP && l2_up) load_row(hup + k * VW, hu[k]);
+                    if (BOT && l2_dn) load_row(hdn + k * VW, hd[k]);
                 }
                 if (++spins > kSpinLimit) __trap();
             }
+            const uint32_t rph = static_cast<uint32_t>(((j - 1) >> 1) & 1);
+            if (TOP && ds_up) mbar_wait(&c.rbar[rq * 2 + 0], rph);
+            if (BOT && ds_dn) mbar_wait(&c.rbar[rq * 2 + 1], rph);
             GD_TADD(1, t_spin);
 #ifdef GD_SWEEP_TRACE
             t_tail0_outer = clock64();
             trc[3] += spins;
 #endif
+            // a DSMEM row: the whole row sits in this CTA's receive buffer
+            auto recv_window = [&](int side, float (&pw)[6]) {
+                const float* rp = c.recv + (rq * 2 + side) * VW;
+                const float4 q4 = *reinterpret_cast<const float4*>(rp + vl);
+                const float c4[kC] = {q4.x, q4.y, q4.z, q4.w};
+                make_window(c4, edge_l ? rp[vl - 1] : INF, edge_r ? rp[vl + kC] : INF, lane, pw);
+                if (!has_left) pw[0] = INF;
+                if (!has_right) pw[5] = INF;
+            };
             if (TOP) {
                 // rows -HROWS .. -1: the neighbour above's last rows
                 float pw1[6], iw1[6];
-                halo_window(hu[HROWS - 1], has_up, has_left, has_right, lane, pw1);
+                if (ds_up) recv_window(0, pw1);
+                else halo_window(hu[HROWS - 1], has_up, has_left, has_right, lane, pw1);
                 i_window(-1, iw1);
                 relax_row<KIND, F64>(acc[0], pw1, iw1, ic[0], -1, p);
                 if (GHOST && has_up) {
@@ -643,7 +687,8 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p,
             if (BOT) {
                 // rows R .. R+HROWS-1: the neighbour below's first rows
                 float pw1[6], iw1[6];
-                halo_window(hd[0], has_dn, has_left, has_right, lane, pw1);
+                if (ds_dn) recv_window(1, pw1);
+                else halo_window(hd[0], has_dn, has_left, has_right, lane, pw1);
                 i_window(R, iw1);
                 relax_row<KIND, F64>(acc[RW - 1], pw1, iw1, ic[RW - 1], +1, p);
                 if (GHOST && has_dn) {
@@ -819,7 +864,7 @@ cudaError_t plane_step_one(const SweepParams& p, int s, int sp, cudaStream_t str
 // last warp is the TMA producer.  Slot j % NST carries plane p(j); it is
 // released ("empty") by every consumer warp during step j+1, which reads it as
 // the previous plane's intensities.
-template <int KIND, bool F64, int RW, int NWU, int NST, int MW, bool TB>
+template <int KIND, bool F64, int RW, int NWU, int NST, int MW, bool TB, bool CL>
 // One CTA per SM: two R = 2 CTAs per SM (126-register cap) measured 1.66 vs
 // 1.25 us/step for R = 4 at 512^3 -- twice the halo links cost more than the
 // second CTA hides (profiles/README.md).
@@ -841,9 +886,11 @@ __global__ void __launch_bounds__((MW * NWU + 1) * 32, MW == 2 && NWU * RW == 4 
     c.si = c.sd + NST * nwv * DBOX;
     c.rows = c.si + NST * nwv * IBOX;
     c.edge = c.rows + 2 * NWU * 2 * nwv * kWV;
-    c.full = reinterpret_cast<uint64_t*>(c.edge + 2 * NWU * nwv * 2 * L::ESL);
+    c.recv = c.edge + 2 * NWU * nwv * 2 * L::ESL;
+    c.full = reinterpret_cast<uint64_t*>(c.recv + (CL ? 2 * 2 * nwv * kWV : 0));
     c.empty = c.full + NST;
-    c.progress = reinterpret_cast<int*>(c.empty + NST);
+    c.rbar = c.empty + NST;
+    c.progress = reinterpret_cast<int*>(c.rbar + 4);
     c.nwv = nwv;
     c.g = blockIdx.x;
     c.b = c.g / p.ntu;
@@ -852,16 +899,20 @@ __global__ void __launch_bounds__((MW * NWU + 1) * 32, MW == 2 && NWU * RW == 4 
     c.n1 = p.ns - 1;
     c.J = p.npass * c.n1;
     c.VW = nwv * kWV;
+    c.rank = CL ? static_cast<int>(cluster_ctarank()) : 0;
 
     if (tid == 0) {
         for (int s = 0; s < NST; ++s) {
             mbar_init(&c.full[s], 1);
             mbar_init(&c.empty[s], ncw);
         }
+        for (int s = 0; s < 4; ++s) mbar_init(&c.rbar[s], 1);
         *c.progress = -1;
         fence_mbar_init();
     }
     __syncthreads();
+    // The neighbours' mbarriers must be initialised before the first remote store.
+    if constexpr (CL) cluster_sync_all();
 
     // ======================= producer warp ==================================
     if (w == ncw) {
@@ -894,6 +945,8 @@ __global__ void __launch_bounds__((MW * NWU + 1) * 32, MW == 2 && NWU * RW == 4 
                 }
             }
         }
+        __syncwarp();
+        if constexpr (CL) cluster_sync_all();  // no CTA leaves while its cluster runs
         return;
     }
 
@@ -910,10 +963,9 @@ __global__ void __launch_bounds__((MW * NWU + 1) * 32, MW == 2 && NWU * RW == 4 
 #define GD_ROLE(T, B)                                                                      \
     if (top == T && bot == B) {                                                            \
         if (full)                                                                          \
-            consumer_loop<KIND, F64, RW, NWU, NST, TB, T, B, true>(p, c, wu, wv, lane);    \
+            consumer_loop<KIND, F64, RW, NWU, NST, TB, CL, T, B, true>(p, c, wu, wv, lane); \
         else                                                                               \
-            consumer_loop<KIND, F64, RW, NWU, NST, TB, T, B, false>(p, c, wu, wv, lane);   \
-        return;                                                                            \
+            consumer_loop<KIND, F64, RW, NWU, NST, TB, CL, T, B, false>(p, c, wu, wv, lane);\
     }
     if (NWU == 1) {
         GD_ROLE(true, true)
@@ -923,18 +975,42 @@ __global__ void __launch_bounds__((MW * NWU + 1) * 32, MW == 2 && NWU * RW == 4 
         if (NWU > 2) GD_ROLE(false, false)
     }
 #undef GD_ROLE
+    __syncwarp();
+    if constexpr (CL) cluster_sync_all();
 }
 
-template <int KIND, bool F64, int RW, int NWU, int NST, int MW, bool TB>
+template <int KIND, bool F64, int RW, int NWU, int NST, int MW, bool TB, bool CL>
 cudaError_t launch_one(const CUtensorMap& tm_d, const CUtensorMap& tm_i, const SweepParams& p,
                        cudaStream_t stream) {
     using L = Layout<RW, NWU, NST, TB>;
-    auto fn = sweep_kernel<KIND, F64, RW, NWU, NST, MW, TB>;
-    const size_t smem = L::smem_bytes(p.nwv);
+    auto fn = sweep_kernel<KIND, F64, RW, NWU, NST, MW, TB, CL>;
+    const size_t smem = L::smem_bytes(p.nwv, CL);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     const int grid = p.nvol * p.ntu;
+    if constexpr (CL) {
+        // Cooperative (co-residency guaranteed) and clustered (DSMEM links).
+        if (p.cs > 8) {
+            e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            if (e != cudaSuccess) return e;
+        }
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3((p.nwv * NWU + 1) * 32);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = stream;
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = static_cast<unsigned>(p.cs);
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        at[1].id = cudaLaunchAttributeCooperative;
+        at[1].val.cooperative = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 2;
+        return cudaLaunchKernelEx(&cfg, fn, tm_d, tm_i, p);
+    }
     void* args[] = {const_cast<CUtensorMap*>(&tm_d), const_cast<CUtensorMap*>(&tm_i),
                     const_cast<SweepParams*>(&p)};
     return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(fn), dim3(grid),
@@ -942,10 +1018,42 @@ cudaError_t launch_one(const CUtensorMap& tm_d, const CUtensorMap& tm_i, const S
                                        args, smem, stream);
 }
 
-template <int KIND, bool F64, int RW, int NWU, int NST, int MW, bool TB>
+template <int KIND, bool F64, int RW, int NWU, int NST, int MW, bool TB, bool CL>
+int coresident_clusters(int nwv, int cs) {
+    using L = Layout<RW, NWU, NST, TB>;
+    auto fn = sweep_kernel<KIND, F64, RW, NWU, NST, MW, TB, CL>;
+    const size_t smem = L::smem_bytes(nwv, true);
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem)) != cudaSuccess ||
+        (cs > 8 &&
+         cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+             cudaSuccess)) {
+        (void)cudaGetLastError();
+        return 0;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs * 64);
+    cfg.blockDim = dim3((nwv * NWU + 1) * 32);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = static_cast<unsigned>(cs);
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return 0;
+    }
+    return n * cs;
+}
+
+template <int KIND, bool F64, int RW, int NWU, int NST, int MW, bool TB, bool CL>
 int coresident(int nwv) {
     using L = Layout<RW, NWU, NST, TB>;
-    auto fn = sweep_kernel<KIND, F64, RW, NWU, NST, MW, TB>;
+    auto fn = sweep_kernel<KIND, F64, RW, NWU, NST, MW, TB, CL>;
     const size_t smem = L::smem_bytes(nwv);
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem)) != cudaSuccess) {
@@ -971,11 +1079,13 @@ int coresident(int nwv) {
 // per scheduler); R = 1 serves single-row planes (2D).  Wide planes (<= 2048
 // columns) trade registers for warps.
 #define GD_SWEEP_CASES(X)                                                                 \
-    X(1, 1, 2, 6, false) X(2, 1, 2, 6, false) X(2, 2, 2, 6, false) X(2, 2, 2, 6, true)      \
-    X(4, 2, 2, 6, false) X(4, 4, 2, 4, false) X(1, 4, 2, 6, false)                          \
-    X(1, 1, 4, 6, false) X(2, 1, 4, 6, false) X(2, 2, 4, GD_NST4, false)                    \
-    X(2, 2, 4, GD_NST4, true) X(4, 2, 4, 6, false) X(1, 4, 4, 6, false)                     \
-    X(1, 1, 16, 6, false) X(2, 1, 16, 6, false) X(4, 1, 16, 6, false)
+    X(1, 1, 2, 6, false, false) X(2, 1, 2, 6, false, false) X(2, 2, 2, 6, false, false)     \
+    X(2, 2, 2, 6, true, false) X(2, 2, 2, 6, false, true)                                   \
+    X(4, 2, 2, 6, false, false) X(4, 4, 2, 4, false, false) X(1, 4, 2, 6, false, false)     \
+    X(1, 1, 4, 6, false, false) X(2, 1, 4, 6, false, false) X(2, 2, 4, GD_NST4, false, false) \
+    X(2, 2, 4, GD_NST4, true, false) X(2, 2, 4, GD_NST4, false, true)                       \
+    X(4, 2, 4, 6, false, false) X(1, 4, 4, 6, false, false)                                 \
+    X(1, 1, 16, 6, false, false) X(2, 1, 16, 6, false, false) X(4, 1, 16, 6, false, false)
 
 int width_class(int nwv) { return nwv <= 2 ? 2 : (nwv <= 4 ? 4 : 16); }
 
@@ -988,8 +1098,8 @@ int g_sweep_rw = -1;
 int preferred_rw(int kind) { return g_sweep_rw >= 0 ? g_sweep_rw : (kind == kBlend ? 1 : 0); }
 // The preferred shape exists for (R, width class, tb)?
 bool rw_pref_exists(int R, int mw, bool tb, int rw) {
-#define GD_CASE(RWW, NW, MM, NS, T) \
-    if (R == RWW * NW && mw == MM && tb == T && RWW == rw) return true;
+#define GD_CASE(RWW, NW, MM, NS, T, C) \
+    if (R == RWW * NW && mw == MM && tb == T && !C && RWW == rw) return true;
     GD_SWEEP_CASES(GD_CASE)
 #undef GD_CASE
     return false;
@@ -1012,20 +1122,23 @@ cudaError_t dispatch_r(int R, bool tb, const CUtensorMap& tm_d, const CUtensorMa
                        const SweepParams& p, cudaStream_t s) {
     const int mw = width_class(p.nwv);
     RwSel sel(R, mw, tb, preferred_rw(KIND));
-#define GD_CASE(RWW, NW, MM, NS, T)                                  \
-    if (R == RWW * NW && mw == MM && tb == T && sel.ok(RWW))         \
-        return launch_one<KIND, F64, RWW, NW, NS, MM, T>(tm_d, tm_i, p, s);
+    const bool cl = p.cs > 1;
+#define GD_CASE(RWW, NW, MM, NS, T, C)                               \
+    if (R == RWW * NW && mw == MM && tb == T && cl == C && sel.ok(RWW)) \
+        return launch_one<KIND, F64, RWW, NW, NS, MM, T, C>(tm_d, tm_i, p, s);
     GD_SWEEP_CASES(GD_CASE)
 #undef GD_CASE
     return cudaErrorInvalidValue;
 }
 
 template <int KIND, bool F64>
-int dispatch_cores(int R, bool tb, int nwv) {
+int dispatch_cores(int R, bool tb, int nwv, int cs) {
     const int mw = width_class(nwv);
     RwSel sel(R, mw, tb, preferred_rw(KIND));
-#define GD_CASE(RWW, NW, MM, NS, T) \
-    if (R == RWW * NW && mw == MM && tb == T && sel.ok(RWW)) return coresident<KIND, F64, RWW, NW, NS, MM, T>(nwv);
+#define GD_CASE(RWW, NW, MM, NS, T, C)                                      \
+    if (R == RWW * NW && mw == MM && tb == T && (cs > 1) == C && sel.ok(RWW))  \
+        return C ? coresident_clusters<KIND, F64, RWW, NW, NS, MM, T, C>(nwv, cs) \
+                 : coresident<KIND, F64, RWW, NW, NS, MM, T, C>(nwv);
     GD_SWEEP_CASES(GD_CASE)
 #undef GD_CASE
     return 0;
@@ -1065,8 +1178,8 @@ void sweep_set_rows_per_warp(int rw) { g_sweep_rw = rw; }
 int sweep_warp_rows(int R, int nwv, int kind) {
     const int mw = width_class(nwv);
     RwSel sel(R, mw, false, preferred_rw(kind));
-#define GD_CASE(RWW, NW, MM, NS, T) \
-    if (R == RWW * NW && mw == MM && !T && sel.ok(RWW)) return NW;
+#define GD_CASE(RWW, NW, MM, NS, T, C) \
+    if (R == RWW * NW && mw == MM && !T && !C && sel.ok(RWW)) return NW;
     GD_SWEEP_CASES(GD_CASE)
 #undef GD_CASE
     return 0;
@@ -1075,22 +1188,32 @@ int sweep_warp_rows(int R, int nwv, int kind) {
 bool sweep_has_tb(int R, int nwv, int kind) {
     const int mw = width_class(nwv);
     RwSel sel(R, mw, true, preferred_rw(kind));
-#define GD_CASE(RWW, NW, MM, NS, T) \
-    if (R == RWW * NW && mw == MM && T && sel.ok(RWW)) return true;
+#define GD_CASE(RWW, NW, MM, NS, T, C) \
+    if (R == RWW * NW && mw == MM && T && !C && sel.ok(RWW)) return true;
     GD_SWEEP_CASES(GD_CASE)
 #undef GD_CASE
     return false;
 }
 
-int sweep_max_coresident(int R, bool tb, int nwv, int kind, bool f64) {
+bool sweep_has_cluster(int R, int nwv, int kind) {
+    const int mw = width_class(nwv);
+    RwSel sel(R, mw, false, preferred_rw(kind));
+#define GD_CASE(RWW, NW, MM, NS, T, C) \
+    if (R == RWW * NW && mw == MM && !T && C && sel.ok(RWW)) return true;
+    GD_SWEEP_CASES(GD_CASE)
+#undef GD_CASE
+    return false;
+}
+
+int sweep_max_coresident(int R, bool tb, int nwv, int kind, bool f64, int cs) {
     switch (kind) {
-        case kSpatial: return dispatch_cores<kSpatial, false>(R, tb, nwv);
+        case kSpatial: return dispatch_cores<kSpatial, false>(R, tb, nwv, cs);
         case kIntensity:
-            return f64 ? dispatch_cores<kIntensity, true>(R, tb, nwv)
-                       : dispatch_cores<kIntensity, false>(R, tb, nwv);
+            return f64 ? dispatch_cores<kIntensity, true>(R, tb, nwv, cs)
+                       : dispatch_cores<kIntensity, false>(R, tb, nwv, cs);
         default:
-            return f64 ? dispatch_cores<kBlend, true>(R, tb, nwv)
-                       : dispatch_cores<kBlend, false>(R, tb, nwv);
+            return f64 ? dispatch_cores<kBlend, true>(R, tb, nwv, cs)
+                       : dispatch_cores<kBlend, false>(R, tb, nwv, cs);
     }
 }
 

@@ -71,6 +71,8 @@ struct SweepParams {
     int first_orient;         // +1 / -1
     int npass;                // 1 or 2 (second pass runs the opposite orientation)
     int fence_turn;           // emit fence.proxy.async on forward stores (npass == 2)
+    int cs;                   // thread-block cluster size: strips of one cluster exchange
+                              // their halo rows through DSMEM (1 = every link via L2)
     uint32_t tag_base;
     unsigned long long* halo; // tagged halo words: [strip][parity][TOP|BOT][nwv*128]
     long long* trace;         // optional per-warp cycle counters (null in production)
@@ -100,8 +102,11 @@ cudaError_t launch_plane_step(int kind, bool f64, const SweepParams& p, int s, i
                               cudaStream_t stream);
 // Experiments: prefer strip shapes with this many rows per warp (-1 = per-kind default).
 void sweep_set_rows_per_warp(int rw);
+// Whether a thread-block-cluster (DSMEM halo) variant exists for this strip shape.
+bool sweep_has_cluster(int R, int nwv, int kind);
 // Whether a temporally blocked variant exists for this strip shape.
 bool sweep_has_tb(int R, int nwv, int kind);
-int sweep_max_coresident(int R, bool tb, int nwv, int kind, bool f64);
+// Co-resident CTAs of the strip shape (cs > 1: in clusters of cs CTAs).
+int sweep_max_coresident(int R, bool tb, int nwv, int kind, bool f64, int cs = 1);
 
 }  // namespace gdb
