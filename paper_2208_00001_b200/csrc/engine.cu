@@ -19,6 +19,7 @@
 #include "aux_kernels.cuh"
 #include "engine.cuh"
 #include "metric_host.hpp"
+#include "rowchain.cuh"
 #include "sweep.cuh"
 
 namespace gdb {
@@ -343,10 +344,12 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
     static const int cs_env =
         std::getenv("GEODIST_SWEEP_CLUSTER") ? std::atoi(std::getenv("GEODIST_SWEEP_CLUSTER")) : -1;
     int cs = 1;
-    const bool cs_default = kind == kIntensity && nwv >= 4 && ntu >= 64;
+    // Spatial (lambda = 0) prefers pairs: 512^3 13.32 (cs 2) / 13.56 (cs 4) / 13.64 ms (L2 only).
+    const bool cs_default = (kind == kIntensity || kind == kSpatial) && nwv >= 4 && ntu >= 64;
     if (R && !tb && ntu > 1 && (cs_env >= 0 || cs_default) && sweep_has_cluster(R, nwv, kind)) {
         const long long ctas = static_cast<long long>(group) * ntu;
-        const int tries[3] = {cs_env >= 0 ? cs_env : 4, cs_env >= 0 ? 0 : 2, 0};
+        const int first = cs_env >= 0 ? cs_env : (kind == kSpatial ? 2 : 4);
+        const int tries[3] = {first, cs_env >= 0 ? 0 : 2, 0};
         for (int cand : tries) {
             if (cand < 2 || cand > 16) continue;
             if (ctas % cand == 0 && sweep_max_coresident(R, false, nwv, kind, f64, cand) >= ctas) {
@@ -381,6 +384,27 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
             p.c0[k] = blend_c0(lambda, rho);
             p.c0_f[k] = static_cast<float>(p.c0[k]);
         }
+
+    // Single-row planes (2D images): the row-chain kernel, one CTA per image
+    // (GEODIST_ROWCHAIN=0 selects the strip kernel's R = 1 shape instead).
+    static const bool rowchain_env =
+        !(std::getenv("GEODIST_ROWCHAIN") && std::atoi(std::getenv("GEODIST_ROWCHAIN")) == 0);
+    if (nu == 1 && nv <= kRowChainMaxWidth && rowchain_env && !force_fallback) {
+        p.ntu = 1;
+        p.image = ibase;
+        for (int b0 = 0; b0 < w.B; b0 += 65535) {
+            p.nvol = std::min(65535, w.B - b0);
+            p.dist = dbase + b0 * vol;
+            p.image = ibase + b0 * vol;
+            const double bytes = static_cast<double>(p.nvol) * g.voxels() * npass *
+                                 (kind == kSpatial ? 8.0 : 12.0);
+            ProfScope ps(kProfSweep, bytes, s);
+            GD_CK(launch_row_chain(kind, f64, p, s));
+            g_launches += 1;
+            if (st) st->kernel_launches += 1;
+        }
+        return Status::Ok();
+    }
 
     if (R == 0) {
         // One launch per plane step (plane_step_kernel), every volume at once.

@@ -20,6 +20,8 @@ CASES = [
     ((20, 70, 132), (1.0, 1.0, 2.5)),
     ((9, 130, 260), (1.0, 1.0, 1.0)),
     ((24, 17, 520), (2.0, 1.0, 1.0)),
+    ((45, 300), (1.0, 1.5)),  # 2D: row-chain kernel (or the strip kernel's R = 1 shape)
+    ((7, 130), (1.0, 1.0)),
 ]
 
 
@@ -41,7 +43,7 @@ def main():
                     print(f"mismatch shape={shape} lam={lam} it={it}: {parity(g, r)}")
                     return 1
             # single directional passes (npass = 1: no backward half)
-            for axis in range(3):
+            for axis in (range(3) if len(shape) == 3 else (1, 2)):
                 for orient in (+1, -1):
                     g = gd.directional_pass(d0, img, axis, orient, sp, lam)
                     r = o.directional_pass(d0, img, axis, orient, sp, lam)

@@ -129,6 +129,34 @@ def test_batched_tall_strips(gd, oracle, lam, shape):
         _check(g[b], r, lam)
 
 
+@pytest.mark.parametrize("lam", LAMBDAS)
+@pytest.mark.parametrize("shape,spacing", [
+    ((2, 9), (1.0, 1.5)),        # one step per pass: the whole backward pass is the turn window
+    ((6, 600), (1.0, 1.0)),      # fewer steps than the prefetch ring
+    ((21, 517), (1.3, 0.7)),     # ragged row (W % 4 != 0), 17 steps: ring + turn window
+    ((300, 2040), (1.0, 2.5)),   # widest row-chain row (510 threads), long chain
+    ((40, 2100), (1.0, 1.0)),    # wider than the row chain: strip kernel R = 1
+], ids=["2x9", "6x600", "21x517", "300x2040", "40x2100"])
+def test_row_chain_2d(gd, oracle, shape, spacing, lam):
+    """2D passes (single-row planes) run the row-chain kernel: one CTA per image,
+    registers + one barrier per step, prefetch ring and turn buffer for the
+    backward half.  Every direction, full scans and the transform."""
+    rng = np.random.default_rng(abs(hash((shape, lam, 5))) % 2**32)
+    img = dyadic_image(rng, shape)
+    d0 = seed_init(rng, shape, 3)
+    for axis in (1, 2):
+        for o in (1, -1):
+            g = gd.directional_pass(d0, img, axis, o, spacing, lam)
+            r = oracle.directional_pass(d0, img, axis, o, spacing, lam)
+            _check(g, r, lam)
+    for it in (1, 2):
+        _check(gd.parallel_scan(img, d0, spacing, lam, it),
+               oracle.parallel_scan(img, d0, spacing, lam, it), lam)
+    m = point_mask(shape)
+    _check(gd.generalized_geodesic(img, m, spacing, lam, 1e10, 2),
+           oracle.generalized_geodesic(img, m, spacing, lam, 1e10, 2), lam)
+
+
 @pytest.mark.parametrize("shape", [(3, 6, 2100), (3, 1300, 600)],
                          ids=["wider_than_2048", "more_strips_than_sms"])
 def test_large_planes_plane_step(gd, oracle, shape):
