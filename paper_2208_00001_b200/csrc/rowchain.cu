@@ -39,8 +39,11 @@ __global__ void __launch_bounds__(512, 1) row_chain_kernel(const __grid_constant
 #pragma unroll
     for (int q = 0; q < kC; ++q) colv[q] = v0 + q < p.nv;
     const bool any = colv[0];
-    float* const dist = p.dist + static_cast<long long>(blockIdx.x) * p.vol_stride + v0;
-    const float* const img = p.image + static_cast<long long>(blockIdx.x) * p.vol_stride + v0;
+    // Threads past the row load column 0 (values unused: outputs masked to +inf),
+    // so the row loads need no per-thread branch.
+    const int v0l = any ? v0 : 0;
+    float* const dist = p.dist + static_cast<long long>(blockIdx.x) * p.vol_stride + v0l;
+    const float* const img = p.image + static_cast<long long>(blockIdx.x) * p.vol_stride + v0l;
     const int n1 = p.ns - 1, J = p.npass * n1;
     auto plane = [&](int j) {
         if (j <= n1) return p.first_orient > 0 ? j : n1 - j;
@@ -51,7 +54,6 @@ __global__ void __launch_bounds__(512, 1) row_chain_kernel(const __grid_constant
     // that plane fewer than kPF steps before step j.
     auto in_turn = [&](int j) { return j > n1 && j <= n1 + kPF; };
     auto ld4 = [&](const float* base, int j) -> float4 {
-        if (!any) return make_float4(INF, INF, INF, INF);
         return *reinterpret_cast<const float4*>(base + static_cast<long long>(plane(j)) * p.ss);
     };
     auto to_arr = [&](float4 v, float (&a)[kC], float fill) {
@@ -91,74 +93,85 @@ __global__ void __launch_bounds__(512, 1) row_chain_kernel(const __grid_constant
     }
     __syncthreads();
 
-    for (int j0 = 1; j0 <= J; j0 += kPF) {
-#pragma unroll
-        for (int u = 0; u < kPF; ++u) {
-            const int j = j0 + u;
-            if (j > J) break;
-            // previous row's neighbours v-1 / v+4
-            const float4* e = edges + ((j - 1) & 1) * nw;
-            float lP = __shfl_up_sync(kFullMask, P[kC - 1], 1);
-            float lI = __shfl_up_sync(kFullMask, PI[kC - 1], 1);
-            float rP = __shfl_down_sync(kFullMask, P[0], 1);
-            float rI = __shfl_down_sync(kFullMask, PI[0], 1);
-            if (lane == 0) {
-                const float4 w = warp > 0 ? e[warp - 1] : make_float4(0.f, 0.f, INF, 0.f);
-                lP = w.z;
-                lI = w.w;
-            }
-            if (lane == kWarpLast) {
-                const float4 w = warp + 1 < nw ? e[warp + 1] : make_float4(INF, 0.f, 0.f, 0.f);
-                rP = w.x;
-                rI = w.y;
-            }
-            const float pw[6] = {lP, P[0], P[1], P[2], P[3], rP};
-            const float iw[6] = {lI, PI[0], PI[1], PI[2], PI[3], rI};
-            float dold[kC], ic[kC];
-            if (in_turn(j)) {
-                const float4 t = *reinterpret_cast<const float4*>(tbuf + (j - n1 - 1) * nvp + v0);
-                to_arr(t, dold, INF);
-            } else {
-                to_arr(Rd[u], dold, INF);
-            }
-            if (kI) to_arr(Ri[u], ic, 0.0f);
-            else
-#pragma unroll
-                for (int q = 0; q < kC; ++q) ic[q] = 0.0f;
-            Acc<KIND, F64> acc[kC];
-#pragma unroll
-            for (int q = 0; q < kC; ++q) acc[q].init(dold[q]);
-            relax_row<KIND, F64>(acc, pw, iw, ic, 0, p);
-            float N[kC];
-#pragma unroll
-            for (int q = 0; q < kC; ++q) N[q] = colv[q] ? acc[q].final(p) : INF;
-            if (any) {
-                float* o = dist + static_cast<long long>(plane(j)) * p.ss;
-                if (colv[kC - 1]) {
-                    *reinterpret_cast<float4*>(o) = make_float4(N[0], N[1], N[2], N[3]);
-                } else {
-#pragma unroll
-                    for (int q = 0; q < kC; ++q)
-                        if (colv[q]) o[q] = N[q];
-                }
-            }
-            save_turn(j, N);
-            put_edges(j, N, ic);
-            // prefetch step j + kPF into the slot just consumed (after the store:
-            // a backward plane outside the turn window was written at a step <= j)
-            const int jn = j + kPF;
-            if (jn <= J) {
-                if (!in_turn(jn)) Rd[u] = ld4(dist, jn);
-                if (kI) Ri[u] = ld4(img, jn);
-            }
-#pragma unroll
-            for (int q = 0; q < kC; ++q) {
-                P[q] = N[q];
-                PI[q] = ic[q];
-            }
-            __syncthreads();
+    // One plane step.  Branch-light (ncu: one warp per scheduler, the step is
+    // issue-latency bound -- branches and masks were 1/3 of the stall samples):
+    // the warp-edge slots and the turn buffer are read unconditionally and
+    // selected; loaded rows are not masked -- a padding column's output is
+    // forced to +inf, so its distance is never a finite candidate and its
+    // intensity only meets +inf distances (inf or NaN candidates; fminf drops NaN).
+    const int wl = warp > 0 ? warp - 1 : 0, wr = warp + 1 < nw ? warp + 1 : warp;
+    const bool has_l = warp > 0, has_r = warp + 1 < nw;
+    const bool full = colv[kC - 1];
+    auto step = [&](int j, float4& rd, float4& ri) {
+        const float4* e = edges + ((j - 1) & 1) * nw;
+        const float4 el = e[wl], er = e[wr];
+        float lP = __shfl_up_sync(kFullMask, P[kC - 1], 1);
+        float lI = __shfl_up_sync(kFullMask, PI[kC - 1], 1);
+        float rP = __shfl_down_sync(kFullMask, P[0], 1);
+        float rI = __shfl_down_sync(kFullMask, PI[0], 1);
+        if (lane == 0) {
+            lP = has_l ? el.z : INF;
+            lI = el.w;
         }
+        if (lane == kWarpLast) {
+            rP = has_r ? er.x : INF;
+            rI = er.y;
+        }
+        const float pw[6] = {lP, P[0], P[1], P[2], P[3], rP};
+        const float iw[6] = {lI, PI[0], PI[1], PI[2], PI[3], rI};
+        int t = j - n1 - 1;
+        const bool turn = t >= 0 && t < kPF;
+        t = t < 0 ? 0 : (t >= kPF ? kPF - 1 : t);
+        const float4 tv = *reinterpret_cast<const float4*>(tbuf + t * nvp + v0);
+        const float4 dv = turn ? tv : rd;
+        const float dold[kC] = {dv.x, dv.y, dv.z, dv.w};
+        float ic[kC] = {0.0f, 0.0f, 0.0f, 0.0f};
+        if (kI) {
+            ic[0] = ri.x;
+            ic[1] = ri.y;
+            ic[2] = ri.z;
+            ic[3] = ri.w;
+        }
+        Acc<KIND, F64> acc[kC];
+#pragma unroll
+        for (int q = 0; q < kC; ++q) acc[q].init(dold[q]);
+        relax_row<KIND, F64>(acc, pw, iw, ic, 0, p);
+        float N[kC];
+#pragma unroll
+        for (int q = 0; q < kC; ++q) N[q] = colv[q] ? acc[q].final(p) : INF;
+        float* o = dist + static_cast<long long>(plane(j)) * p.ss;
+        if (full) {
+            *reinterpret_cast<float4*>(o) = make_float4(N[0], N[1], N[2], N[3]);
+        } else if (any) {
+#pragma unroll
+            for (int q = 0; q < kC; ++q)
+                if (colv[q]) o[q] = N[q];
+        }
+        save_turn(j, N);
+        put_edges(j, N, ic);
+        // prefetch step j + kPF into the slot just consumed (after the store:
+        // a backward plane outside the turn window was written at a step <= j)
+        const int jn = j + kPF;
+        if (jn <= J) {
+            if (!in_turn(jn)) rd = ld4(dist, jn);
+            if (kI) ri = ld4(img, jn);
+        }
+#pragma unroll
+        for (int q = 0; q < kC; ++q) {
+            P[q] = N[q];
+            PI[q] = ic[q];
+        }
+        __syncthreads();
+    };
+
+    int j0 = 1;
+    for (; j0 + kPF - 1 <= J; j0 += kPF) {
+#pragma unroll
+        for (int u = 0; u < kPF; ++u) step(j0 + u, Rd[u], Ri[u]);
     }
+#pragma unroll
+    for (int u = 0; u < kPF; ++u)
+        if (j0 + u <= J) step(j0 + u, Rd[u], Ri[u]);
 }
 
 template <int KIND, bool F64>
