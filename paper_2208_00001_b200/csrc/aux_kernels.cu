@@ -93,17 +93,30 @@ __global__ void init_check_kernel(VolView mv, VolView dv, const float* img, cons
     const long long t0 = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
     if (dense(mv) && dense(dv) && (n & 3) == 0) {
         const long long n4 = n >> 2;
-        for (long long i = t0; i < n4; i += stride) {
-            const float4 m = reinterpret_cast<const float4*>(mask)[i];
+        // Two float4 per stream in flight per thread (all loads issued first):
+        // 0.37 ms at 512^3 with one, a 3-stream read/read/write copy.
+        auto one = [&](const float4 m, const float4 a, long long i) {
             bad |= !(m.x >= 0.0f && m.x <= 1.0f) | !(m.y >= 0.0f && m.y <= 1.0f) |
                    !(m.z >= 0.0f && m.z <= 1.0f) | !(m.w >= 0.0f && m.w <= 1.0f);
             reinterpret_cast<float4*>(dist)[i] = make_float4(
                 init_value(m.x, nu), init_value(m.y, nu), init_value(m.z, nu), init_value(m.w, nu));
             if (img) {
-                const float4 a = reinterpret_cast<const float4*>(img)[i];
                 st.add(a.x); st.add(a.y); st.add(a.z); st.add(a.w);
             }
+        };
+        const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        long long i = t0;
+        for (; i + stride < n4; i += 2 * stride) {
+            const float4 m0 = __ldcs(reinterpret_cast<const float4*>(mask) + i);
+            const float4 m1 = __ldcs(reinterpret_cast<const float4*>(mask) + i + stride);
+            const float4 a0 = img ? reinterpret_cast<const float4*>(img)[i] : z4;
+            const float4 a1 = img ? reinterpret_cast<const float4*>(img)[i + stride] : z4;
+            one(m0, a0, i);
+            one(m1, a1, i + stride);
         }
+        if (i < n4)
+            one(__ldcs(reinterpret_cast<const float4*>(mask) + i),
+                img ? reinterpret_cast<const float4*>(img)[i] : z4, i);
     } else {
         for (long long i = t0; i < n; i += stride) {
             const long long om = vox_offset(mv, i);
