@@ -9,7 +9,8 @@
 // double-buffered shared-memory slot, so a plane step is one relax of 4 voxels
 // plus ONE barrier -- no inter-CTA hand-off at all (the persistent strip kernel
 // pays a TMA ring round trip and a producer warp per step for a row that is
-// only 2 KB).  Rows ahead are prefetched into a register ring PF steps deep.
+// only 2 KB).  Rows ahead are prefetched PF steps deep into a shared-memory
+// ring by cp.async.
 // The backward pass reads the forward pass's output, written by the same
 // thread: loads of it are issued after the store (program order), and the PF
 // planes nearest the turn -- not yet written when their prefetch would issue --
@@ -25,6 +26,19 @@ namespace {
 
 constexpr int kPF = 8;  // prefetch depth (steps)
 
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)),
+                 "l"(gsrc)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 template <int KIND, bool F64>
 __global__ void __launch_bounds__(512, 1) row_chain_kernel(const __grid_constant__ SweepParams p) {
     constexpr bool kI = KIND != kSpatial;
@@ -33,6 +47,8 @@ __global__ void __launch_bounds__(512, 1) row_chain_kernel(const __grid_constant
     const int nw = blockDim.x >> 5, nvp = blockDim.x * kC;
     float4* edges = smem4;                                       // [2 parities][nw]: {P0, I0, P3, I3}
     float* tbuf = reinterpret_cast<float*>(smem4 + 2 * nw);      // [kPF][nvp] turn buffer
+    float* ringd = tbuf + kPF * nvp;                             // [kPF][nvp] prefetched distances
+    float* ringi = ringd + kPF * nvp;                            // [kPF][nvp] prefetched intensities
     const float INF = finf();
     const int v0 = tid * kC;
     bool colv[kC];
@@ -74,7 +90,16 @@ __global__ void __launch_bounds__(512, 1) row_chain_kernel(const __grid_constant
     };
 
     float P[kC], PI[kC];
-    float4 Rd[kPF], Ri[kPF];
+    // Prefetch ring in shared memory, filled by cp.async (no registers: a
+    // register ring made ptxas copy each loaded value right after its load,
+    // waiting on it at once -- 13% long_sb stalls).  One commit group per step.
+    auto fetch = [&](int j, int u) {
+        if (j <= J) {
+            if (!in_turn(j)) cp_async16(ringd + u * nvp + v0, dist + static_cast<long long>(plane(j)) * p.ss);
+            if (kI) cp_async16(ringi + u * nvp + v0, img + static_cast<long long>(plane(j)) * p.ss);
+        }
+        cp_async_commit();
+    };
     // step 0: the first plane is final as loaded
     {
         float4 d0 = ld4(dist, 0), i0 = kI ? ld4(img, 0) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -84,13 +109,7 @@ __global__ void __launch_bounds__(512, 1) row_chain_kernel(const __grid_constant
         put_edges(0, P, PI);
     }
 #pragma unroll
-    for (int u = 0; u < kPF; ++u) {
-        const int j = 1 + u;
-        if (j <= J) {
-            if (!in_turn(j)) Rd[u] = ld4(dist, j);
-            if (kI) Ri[u] = ld4(img, j);
-        }
-    }
+    for (int u = 0; u < kPF; ++u) fetch(1 + u, u);
     __syncthreads();
 
     // One plane step.  Branch-light (ncu: one warp per scheduler, the step is
@@ -102,7 +121,10 @@ __global__ void __launch_bounds__(512, 1) row_chain_kernel(const __grid_constant
     const int wl = warp > 0 ? warp - 1 : 0, wr = warp + 1 < nw ? warp + 1 : warp;
     const bool has_l = warp > 0, has_r = warp + 1 < nw;
     const bool full = colv[kC - 1];
-    auto step = [&](int j, float4& rd, float4& ri) {
+    auto step = [&](int j, int u) {
+        cp_async_wait<kPF - 1>();  // this step's group (committed kPF groups ago) has landed
+        const float4 rd = *reinterpret_cast<const float4*>(ringd + u * nvp + v0);
+        const float4 ri = kI ? *reinterpret_cast<const float4*>(ringi + u * nvp + v0) : make_float4(0.f, 0.f, 0.f, 0.f);
         const float4* e = edges + ((j - 1) & 1) * nw;
         const float4 el = e[wl], er = e[wr];
         float lP = __shfl_up_sync(kFullMask, P[kC - 1], 1);
@@ -151,11 +173,7 @@ __global__ void __launch_bounds__(512, 1) row_chain_kernel(const __grid_constant
         put_edges(j, N, ic);
         // prefetch step j + kPF into the slot just consumed (after the store:
         // a backward plane outside the turn window was written at a step <= j)
-        const int jn = j + kPF;
-        if (jn <= J) {
-            if (!in_turn(jn)) rd = ld4(dist, jn);
-            if (kI) ri = ld4(img, jn);
-        }
+        fetch(j + kPF, u);
 #pragma unroll
         for (int q = 0; q < kC; ++q) {
             P[q] = N[q];
@@ -167,18 +185,18 @@ __global__ void __launch_bounds__(512, 1) row_chain_kernel(const __grid_constant
     int j0 = 1;
     for (; j0 + kPF - 1 <= J; j0 += kPF) {
 #pragma unroll
-        for (int u = 0; u < kPF; ++u) step(j0 + u, Rd[u], Ri[u]);
+        for (int u = 0; u < kPF; ++u) step(j0 + u, u);
     }
 #pragma unroll
     for (int u = 0; u < kPF; ++u)
-        if (j0 + u <= J) step(j0 + u, Rd[u], Ri[u]);
+        if (j0 + u <= J) step(j0 + u, u);
 }
 
 template <int KIND, bool F64>
 cudaError_t launch_one(const SweepParams& p, cudaStream_t s) {
     const int threads = ((p.nv + kC - 1) / kC + 31) / 32 * 32;
     const int nw = threads / 32;
-    const size_t smem = 2 * nw * sizeof(float4) + static_cast<size_t>(kPF) * threads * kC * 4;
+    const size_t smem = 2 * nw * sizeof(float4) + 3 * static_cast<size_t>(kPF) * threads * kC * 4;
     if (smem > 48 * 1024) {  // per device: set on every wide launch (cheap)
         const cudaError_t e = cudaFuncSetAttribute(
             row_chain_kernel<KIND, F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
