@@ -157,6 +157,21 @@ def test_row_chain_2d(gd, oracle, shape, spacing, lam):
            oracle.generalized_geodesic(img, m, spacing, lam, 1e10, 2), lam)
 
 
+@pytest.mark.parametrize("lam", LAMBDAS)
+def test_row_chain_batched_2d(gd, oracle, lam):
+    """A batch of 2D images: one row-chain CTA per image in the same launch."""
+    rng = np.random.default_rng(31)
+    B, shape = 5, (33, 70)
+    imgs = dyadic_image(rng, (B,) + shape)
+    masks = np.ones((B,) + shape, np.float32)
+    for b in range(B):
+        masks[b].reshape(-1)[rng.integers(0, masks[b].size)] = 0.0
+    sp = (1.0, 1.5)
+    g = gd.generalized_geodesic_batched(imgs, masks, sp, lam, 1e10, 2)
+    for b in range(B):
+        _check(g[b], oracle.generalized_geodesic(imgs[b], masks[b], sp, lam, 1e10, 2), lam)
+
+
 @pytest.mark.parametrize("shape", [(3, 6, 2100), (3, 1300, 600)],
                          ids=["wider_than_2048", "more_strips_than_sms"])
 def test_large_planes_plane_step(gd, oracle, shape):
