@@ -1,20 +1,34 @@
 #!/usr/bin/env python
-"""Benchmark: generalised_geodesic3d on 512^3, spacing (1,1,2.5), lambda=1, v=1e10, it=4.
+"""Benchmark: generalised_geodesic3d, inputs resident in HBM, one process per GPU.
 
-Contract:
-  * a step = one generalized_geodesic transform (soft-mask init + 24 directional
-    passes) of one 512^3 volume per GPU; N GPUs = N independent volumes
-    (weak scaling, no collective on the scan);
-  * `value` = total voxels / device time (CUDA events, max over ranks), inputs
-    resident in HBM; every volume (1.5 GB of image+mask+dist) exceeds the 126 MB
-    L2, so no flush is needed between steps;
-  * `e2e` = the same transform through the public C-ABI with pinned HOST buffers:
+Configs (BASELINE.json):
+  * ``--config 512`` (default; the headline): 512^3 float32, spacing
+    (1, 1, 2.5), lambda = 1, v = 1e10, it = 4, point-seed soft mask; one volume
+    per GPU, so N GPUs = a batch of N independent volumes (weak scaling).
+  * ``--config batch64``: the batched config, 64 volumes of 256x256x160 sharded
+    by volume across the N ranks (strong scaling: 64 volumes in total); each
+    rank runs its shard as one batched transform.
+A step = one generalized_geodesic transform (soft-mask init + 24 directional
+passes) of every volume this rank owns.  ``value`` = all ranks' voxels / the
+max over ranks of the CUDA-event step time (paper_2208_00001_b200.shard.run_sharded);
+every working set exceeds the 126 MB L2 (1.5 GB per 512^3 volume; 64 x 40 MB
+per batch array), so no flush is needed between steps.  No collective touches
+the data path; NCCL carries only the barrier and the timing reduction.
+
+Keys beyond the base contract:
+  * ``e2e``: the same transform through the public C-ABI entry
+    (gd_generalized_geodesic_batched, GD_MEM_HOST) with pinned host buffers:
     H2D of image + mask and D2H of the distance map inside the timed region;
-  * `roofline` = the directional-pass kernel's algorithmic 12 B/voxel/pass over
-    its CUDA-event launch time, against MEASURED_PEAKS.json hbm_gbs;
-  * `cpu_baseline` = the unmodified reference (oracle/_ref) on this host's cores,
-    also used for a full-size parity check of the GPU result.
-`--impl reference` times the reference CPU library alone (rank 0).
+  * ``roofline``: the directional-pass kernel's algorithmic 12 B/voxel/pass over
+    its CUDA-event launch time (events on the launching stream), against
+    MEASURED_PEAKS.json hbm_gbs;
+  * ``cpu_baseline`` (rank 0, N = 1): the unmodified reference (oracle/_ref) on
+    this host's cores, median of 3 after 1 warm-up on the same inputs;
+  * ``parity`` (rank 0, any N): the GPU result of rank 0's first volume against
+    the reference's on the same inputs, per voxel (1e-6 abs + 1e-5 rel, bit-exact
+    fraction).
+``--impl reference`` times the reference CPU library alone (rank 0 only) on the
+same config: each step one full volume (512) or a 2-volume sample (batch64).
 """
 from __future__ import annotations
 
@@ -31,21 +45,27 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-SHAPE = (512, 512, 512)
-SPACING = (1.0, 1.0, 2.5)
 NU = 1e10
 ITERS = 4
-METRIC = "Gvoxels/sec generalised_geodesic3d 512^3 it=4"
 UNIT = "Gvoxels/s"
+CONFIGS = {
+    "512": dict(shape=(512, 512, 512), spacing=(1.0, 1.0, 2.5), total=None,
+                metric="Gvoxels/sec generalised_geodesic3d 512^3 it=4", ref_sample=1),
+    "batch64": dict(shape=(256, 256, 160), spacing=(1.0, 1.0, 1.0), total=64,
+                    metric="Gvoxels/sec batched generalised_geodesic3d 64 x 256x256x160 it=4",
+                    ref_sample=2),
+}
 
 
 def bench_seed(ndim: int, size: int) -> int:
+    # tools/main.cpp:312-314
     return 0x67656F64697374 ^ (ndim << 32) ^ size
 
 
-def volume_seed(b: int) -> int:
-    # volume 0 uses the reference CLI's seed (tools/main.cpp:312-314); volume b adds b
-    return bench_seed(3, 512) + b
+def volume_seed(cfg: str, b: int) -> int:
+    # volume 0 of the 512 config uses the reference CLI's seed; volume b adds b
+    size = 512 if cfg == "512" else 256
+    return bench_seed(3, size) + b
 
 
 def host_image(shape, seed):
@@ -139,51 +159,69 @@ class ClockSampler:
 
 
 def cpu_info():
-    model = ""
     try:
         for line in open("/proc/cpuinfo"):
             if line.startswith("model name"):
-                model = line.split(":", 1)[1].strip()
-                break
+                return line.split(":", 1)[1].strip()
     except Exception:
         pass
-    return model
+    return ""
+
+
+def workload_text(cfg, lam, per_gpu):
+    c = CONFIGS[cfg]
+    d, h, w = c["shape"]
+    sp = ",".join(f"{x:g}" for x in c["spacing"])
+    if cfg == "512":
+        return (f"generalised_geodesic3d {d}x{h}x{w}, spacing ({sp}), lambda={lam:g}, v=1e10, "
+                f"it={ITERS}, point seed, one volume per GPU")
+    return (f"batched generalised_geodesic3d {c['total']} x {d}x{h}x{w}, spacing ({sp}), "
+            f"lambda={lam:g}, v=1e10, it={ITERS}, point seed, sharded by volume")
 
 
 def run_reference_arm(args, rank):
-    """bench.py --impl reference: the unmodified reference on this host's cores."""
+    """bench.py --impl reference: the unmodified reference on this host's cores,
+    on the same config as our arm (full volumes; batch64: a 2-volume sample)."""
     if rank != 0:
         return 0
     from oracle.pyoracle import REF_SO, RefLib
+    c = CONFIGS[args.config]
     if not os.path.exists(REF_SO):
         print(json.dumps({"impl": "reference", "unavailable": f"{REF_SO} not built"}))
         return 0
     ref = RefLib()
     cores = os.cpu_count() or 1
-    depth = 128  # bounded sample: a 128-plane slab of the same volume
-    img = host_image(SHAPE, volume_seed(0))[:depth].copy()
-    mask = point_mask_np(SHAPE)[:depth].copy()
-    mask[depth // 2, SHAPE[1] // 2, SHAPE[2] // 2] = 0.0
-    for _ in range(args.warmup):
-        ref.generalized_geodesic(img, mask, SPACING, args.lam, NU, ITERS, workers=cores)
+    nvol = c["ref_sample"]
+    vols = [(host_image(c["shape"], volume_seed(args.config, b)), point_mask_np(c["shape"]))
+            for b in range(nvol)]
+
+    def step():
+        for img, mask in vols:
+            ref.generalized_geodesic(img, mask, c["spacing"], args.lam, NU, ITERS, workers=cores)
+
+    for _ in range(max(args.warmup, 1)):
+        step()
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        ref.generalized_geodesic(img, mask, SPACING, args.lam, NU, ITERS, workers=cores)
+        step()
         times.append(time.perf_counter() - t0)
-    t = sum(times) / len(times)
-    vox = img.size
+    t = statistics.median(times)
+    vox = nvol * float(np.prod(c["shape"]))
     value = vox / t / 1e9
-    sample = (f"{depth}x512x512 slab of the 512^3 workload (same image, spacing, lambda={args.lam}, "
-              f"v=1e10, it=4, point seed), mean of {args.steps} after {args.warmup} warm-up")
+    sample = (f"{nvol} full volume(s) of the workload per step (same SplitMix64 images, spacing, "
+              f"lambda={args.lam:g}, v=1e10, it={ITERS}, point seed); median of {args.steps} "
+              f"after {max(args.warmup, 1)} warm-up")
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (SplitMix64 image, point-seed soft mask)",
-        "config": {"workload": f"generalised_geodesic3d {depth}x512x512 slab, spacing (1,1,2.5), "
-                               f"lambda={args.lam}, v=1e10, it=4",
-                   "engine": "reference geodist::generalized_geodesic, Engine::Parallel (OpenMP)"},
+        "impl": "reference", "metric": c["metric"], "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "ms_per_step_mean": 1e3 * sum(times) / len(times),
+        "higher_is_better": True, "scaling": "weak" if args.config == "512" else "strong",
+        "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (SplitMix64 image on the 2^-24 grid, point-seed soft mask)",
+        "config": {"workload": workload_text(args.config, args.lam, c["total"] or 1),
+                   "engine": "reference geodist::generalized_geodesic, Engine::Parallel (OpenMP), "
+                             "oracle/_ref built from /root/reference with its own flags"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
                          "sample": sample, "cpu": cpu_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -198,8 +236,9 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="512", choices=sorted(CONFIGS))
     ap.add_argument("--lam", type=float, default=1.0)
-    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline / parity leg")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline / parity legs")
     ap.add_argument("--e2e-steps", type=int, default=None)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -212,63 +251,62 @@ def main():
         return run_reference_arm(args, rank)
 
     import torch
-    import paper_2208_00001_b200 as gd
 
+    import paper_2208_00001_b200 as gd
+    from paper_2208_00001_b200.shard import (CudaTimer, max_over_ranks, run_sharded,
+                                             volumes_for_rank)
+
+    c = CONFIGS[args.config]
+    shape, spacing = c["shape"], c["spacing"]
     torch.cuda.set_device(local)
     gd.device.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
-    def barrier():
-        if dist is not None:
-            dist.barrier()
-
     dev = torch.device("cuda", local)
-    img = torch.empty(SHAPE, dtype=torch.float32, device=dev)
-    gd.device.fill_splitmix(img, volume_seed(rank))
-    mask = torch.ones(SHAPE, dtype=torch.float32, device=dev)
-    mask[tuple(s // 2 for s in SHAPE)] = 0.0
+
+    total = c["total"] or world
+    mine = list(volumes_for_rank(total, world, rank))
+    nv = len(mine)
+    batched = nv > 1
+    full = (nv,) + shape if batched else shape
+    img = torch.empty(full, dtype=torch.float32, device=dev)
+    for i, b in enumerate(mine):
+        gd.device.fill_splitmix(img[i] if batched else img, volume_seed(args.config, b))
+    mask = torch.ones(full, dtype=torch.float32, device=dev)
+    for i in range(nv):
+        (mask[i] if batched else mask)[tuple(s // 2 for s in shape)] = 0.0
     out = torch.empty_like(img)
+    vox_rank = nv * float(np.prod(shape))
 
     def step():
-        gd.device.generalized_geodesic(img, mask, out, SPACING, args.lam, NU, ITERS)
+        gd.device.generalized_geodesic(img, mask, out, spacing, args.lam, NU, ITERS,
+                                       batch=nv if batched else None)
 
     clk = ClockSampler(list(range(max(world, 1)))) if rank == 0 else None
     if clk:
         clk.start()
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    barrier()
+    marks = {}
 
-    n0 = gd.kernel_launches()
-    gd.profile_read(reset=True)
-    gd.profile_enable(True)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    barrier()
-    if clk:
-        clk.mark_start()
-    e0.record()
-    for _ in range(args.steps):
-        step()
-    e1.record()
-    torch.cuda.synchronize()
-    if clk:
-        clk.mark_end()
-    barrier()
-    gd.profile_enable(False)
-    prof = gd.profile_read(reset=True)
-    launches = gd.kernel_launches() - n0
-    ms = e0.elapsed_time(e1) / args.steps
-    ms_t = torch.tensor([ms], device=dev, dtype=torch.float64)
-    if dist is not None:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
-    vox = float(np.prod(SHAPE))
-    value = world * vox / (ms_max * 1e-3) / 1e9
+    def on_start():
+        marks["n0"] = gd.kernel_launches()
+        gd.profile_read(reset=True)
+        gd.profile_enable(True)
+        if clk:
+            clk.mark_start()
+
+    def on_end():
+        if clk:
+            clk.mark_end()
+        gd.profile_enable(False)
+        marks["prof"] = gd.profile_read(reset=True)
+        marks["launches"] = gd.kernel_launches() - marks["n0"]
+
+    res = run_sharded(step, vox_rank, args.steps, args.warmup, timer=CudaTimer(), device=dev,
+                      on_start=on_start, on_end=on_end)
+    ms, ms_max, value = res["ms_rank"], res["ms_max"], res["gvox_per_s"]
+    prof, launches = marks["prof"], marks["launches"]
 
     # ---- roofline of the dominant kernel (the directional-pass sweep) ------
     peak, peak_kind = peak_hbm()
@@ -276,105 +314,99 @@ def main():
     achieved = (sw_bytes / sw_n) / (sw_ms / sw_n * 1e-3) / 1e9 if sw_n else 0.0
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_sweep_traffic.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and args.config == "512":
         try:
             traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    step_ms_profiled = sum(v[0] for v in prof.values()) / args.steps
     roofline = {
         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
         "frac": achieved / peak if peak else None, "traffic": traffic,
         "peak_source": f"{peak_kind} MEMORY copy (MEASURED_PEAKS.json hbm_gbs)",
         "kernel": "sweep_kernel (one launch = forward+backward pass pair on one axis)",
         "algorithmic_bytes_per_launch": sw_bytes / sw_n if sw_n else None,
+        "bytes_rule": "12 B per voxel per pass (read image, read distance, write distance)",
         "launch_ms": sw_ms / sw_n if sw_n else None,
         "share_of_step": (sw_ms / args.steps) / ms if ms else None,
         "per_class_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
-        "step_ms_sum_of_launches": step_ms_profiled,
+        "whole_transform_frac": (12.0 * 6 * ITERS * vox_rank / (ms * 1e-3) / 1e9) / peak,
     }
 
     # ---- end to end through the C-ABI with pinned host buffers --------------
+    import ctypes as C
     e2e_steps = args.e2e_steps or min(args.steps, 5)
-    h_img = torch.empty(SHAPE, dtype=torch.float32, pin_memory=True)
-    h_mask = torch.empty(SHAPE, dtype=torch.float32, pin_memory=True)
-    h_out = torch.empty(SHAPE, dtype=torch.float32, pin_memory=True)
+    h_img = torch.empty(full, dtype=torch.float32, pin_memory=True)
+    h_mask = torch.empty(full, dtype=torch.float32, pin_memory=True)
+    h_out = torch.empty(full, dtype=torch.float32, pin_memory=True)
     h_img.copy_(img.cpu())
     h_mask.copy_(mask.cpu())
-    import ctypes as C
     L = gd.lib()
-    grid = gd._grid(SHAPE, SPACING)
+    grid = gd._grid(shape, spacing)
 
     def e2e_step():
-        rc = L.gd_generalized_geodesic(C.byref(grid), C.c_void_p(h_img.data_ptr()),
-                                       C.c_void_p(h_mask.data_ptr()), args.lam, NU, ITERS,
-                                       C.c_void_p(h_out.data_ptr()), gd.GD_MEM_HOST, None, None)
+        rc = L.gd_generalized_geodesic_batched(
+            C.byref(grid), nv, C.c_void_p(h_img.data_ptr()), C.c_void_p(h_mask.data_ptr()),
+            args.lam, NU, ITERS, C.c_void_p(h_out.data_ptr()), gd.GD_MEM_HOST, None, None)
         gd._check(rc)
 
-    e2e_step()
-    torch.cuda.synchronize()
-    barrier()
-    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    f0.record()
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        e2e_step()
-    f1.record()
-    torch.cuda.synchronize()
-    wall = (time.perf_counter() - t0) / e2e_steps
-    e2e_ms = f0.elapsed_time(f1) / e2e_steps
-    e_t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
-    if dist is not None:
-        dist.all_reduce(e_t, op=dist.ReduceOp.MAX)
-    e2e_ms = float(e_t.item())
-    e2e = {"value": world * vox / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,
-           "h2d_bytes_per_step": 2 * int(vox) * 4, "d2h_bytes_per_step": int(vox) * 4,
-           "ms_per_step": e2e_ms, "wall_ms_per_step": wall * 1e3, "steps": e2e_steps,
-           "path": "gd_generalized_geodesic(GD_MEM_HOST) with pinned host buffers"}
+    e2e_res = run_sharded(e2e_step, vox_rank, e2e_steps, 1, timer=CudaTimer(), device=dev)
+    e2e = {"value": e2e_res["gvox_per_s"], "unit": UNIT,
+           "h2d_bytes_per_step": 2 * int(vox_rank) * 4, "d2h_bytes_per_step": int(vox_rank) * 4,
+           "ms_per_step": e2e_res["ms_max"], "steps": e2e_steps,
+           "path": "gd_generalized_geodesic_batched(GD_MEM_HOST) with pinned host buffers"}
 
-    # ---- CPU baseline (reference on this host) + full-size parity -----------
+    # ---- CPU baseline (reference on this host, N = 1) + parity (rank 0) -----
     cpu_baseline, parity = None, None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and not args.no_cpu:
         from oracle.pyoracle import REF_SO, RefLib
         from tests.helpers import parity as parity_fn
+        cores = os.cpu_count() or 1
         if os.path.exists(REF_SO):
             ref = RefLib()
-            cores = os.cpu_count() or 1
-            himg = h_img.numpy()
-            hmask = h_mask.numpy()
-            # the GPU result for exactly these inputs
-            gpu_out = out.cpu().numpy()
-            t0 = time.perf_counter()
-            ref_out = ref.generalized_geodesic(himg, hmask, SPACING, args.lam, NU, ITERS,
-                                               workers=cores)
-            t_ref = time.perf_counter() - t0
-            cpu_baseline = {"value": vox / t_ref / 1e9, "unit": UNIT, "cores": cores,
-                            "kind": "reference",
-                            "sample": "one full 512^3 transform (same inputs, lambda, it=4), "
-                                      "single timed run incl. first-call effects",
-                            "cpu": cpu_info(), "seconds": t_ref}
+            himg = (h_img[0] if batched else h_img).numpy()
+            hmask = (h_mask[0] if batched else h_mask).numpy()
+            gpu_out = (out[0] if batched else out).cpu().numpy()
+            runs = 1 + (3 if world == 1 else 0)  # 1 warm-up + 3 timed, N = 1 only
+            times, ref_out = [], None
+            for i in range(runs):
+                t0 = time.perf_counter()
+                ref_out = ref.generalized_geodesic(himg, hmask, spacing, args.lam, NU, ITERS,
+                                                   workers=cores)
+                if i > 0:
+                    times.append(time.perf_counter() - t0)
+            if times:
+                t_ref = statistics.median(times)
+                cpu_baseline = {"value": float(np.prod(shape)) / t_ref / 1e9, "unit": UNIT,
+                                "cores": cores, "kind": "reference",
+                                "sample": f"one full {'x'.join(map(str, shape))} volume of the "
+                                          "workload (same inputs, lambda, it=4), median of 3 "
+                                          "after 1 warm-up",
+                                "cpu": cpu_info(), "seconds": t_ref,
+                                "seconds_all": [round(t, 3) for t in times]}
             ok, exact, max_abs, max_rel = parity_fn(gpu_out, ref_out)
-            parity = {"vs": "reference (oracle/_ref) at 512^3", "within_tolerance": ok,
-                      "bit_exact_fraction": exact, "max_abs": max_abs, "max_rel": max_rel,
-                      "tolerance": "1e-6 abs + 1e-5 rel, sentinels exact"}
-        else:
-            cpu_baseline = {"value": None, "unit": UNIT, "cores": os.cpu_count(),
-                            "kind": "reference", "sample": "unavailable: oracle/_ref not built"}
+            parity = {"vs": f"reference (oracle/_ref), rank 0 volume {mine[0]}",
+                      "within_tolerance": ok, "bit_exact_fraction": exact, "max_abs": max_abs,
+                      "max_rel": max_rel, "tolerance": "1e-6 abs + 1e-5 rel, sentinels exact"}
+        elif world == 1:
+            cpu_baseline = {"value": None, "unit": UNIT, "cores": cores, "kind": "reference",
+                            "sample": "unavailable: oracle/_ref not built"}
 
     clocks = None
     if clk:
         clk.stop()
         clocks = clk.summary()
+    launches = int(max_over_ranks(launches, dev))
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "metric": c["metric"], "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": "weak" if args.config == "512" else "strong",
+            "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (SplitMix64 image on the 2^-24 grid, point-seed soft mask)",
-            "config": {"workload": "generalised_geodesic3d 512x512x512, spacing (1,1,2.5), "
-                                   f"lambda={args.lam}, v=1e10, it=4, one volume per GPU",
-                       "l2": "inputs larger than L2 (1.5 GB per volume), no flush",
-                       "parallelism": f"volume-sharded x{world}"},
+            "config": {"workload": workload_text(args.config, args.lam, nv),
+                       "volumes_total": total, "volumes_rank0": nv,
+                       "l2": "inputs larger than L2 (no flush)",
+                       "parallelism": f"volume-sharded x{world}, no collective on the scan"},
             "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks, "parity": parity,
         }

@@ -109,6 +109,27 @@ int gd_profile_read(double* ms4, long long* count4, double* bytes4, int reset);
  * gd_profile_read (call it with reset = 0 first); returns the number logged. */
 int gd_profile_log(int* kinds, float* ms, int max);
 
+/* Launch log of the directional-pass kernels, one record per launch group in
+ * launch order (at most 4096 kept): which kernel variant actually ran, so tests
+ * can assert that the intended one did.  Copies up to `max` records into `out`,
+ * returns how many are logged; `reset` != 0 clears the log afterwards. */
+typedef struct gd_launch_rec {
+    int axis;  /* 0 depth, 1 height, 2 width (x-sweep layout) */
+    int npass; /* 1 = one directional pass, 2 = forward+backward pair */
+    int kind;  /* 0 spatial (lambda 0), 1 intensity (lambda 1), 2 blend */
+    int f64;   /* f64 arithmetic path */
+    int path;  /* 0 persistent strip kernel, 1 row chain (2D), 2 plane-step fallback */
+    int rows;  /* rows per strip */
+    int nwv;   /* warp columns per strip */
+    int nwu;   /* warp rows per strip */
+    int cs;    /* thread-block cluster size (1: halo links through L2 only) */
+    int ntu;   /* strips per volume */
+    int nvol;  /* volumes in the launch */
+    int grid;  /* CTAs */
+    int tb;    /* temporally blocked variant (halo exchanged every two planes) */
+} gd_launch_rec;
+int gd_debug_launch_log(gd_launch_rec* out, int max, int reset);
+
 /* Utilities. */
 /* Selects the CUDA device for this thread's subsequent calls (the library
  * carries its own CUDA runtime state; a caller's cudaSetDevice does not reach it). */

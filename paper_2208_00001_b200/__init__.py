@@ -56,6 +56,11 @@ class gd_grid(C.Structure):
     _fields_ = [("ndim", C.c_int), ("dims", C.c_int * 3), ("spacing", C.c_double * 3)]
 
 
+class gd_launch_rec(C.Structure):
+    _fields_ = [(n, C.c_int) for n in ("axis", "npass", "kind", "f64", "path", "rows", "nwv",
+                                       "nwu", "cs", "ntu", "nvol", "grid", "tb")]
+
+
 class gd_stats(C.Structure):
     _fields_ = [("rounds", C.c_int), ("converged", C.c_int), ("complement_empty", C.c_int),
                 ("last_change", C.c_double), ("kernel_launches", C.c_longlong)]
@@ -86,6 +91,7 @@ def lib():
         L.gd_fill_splitmix.argtypes = [fp, C.c_longlong, C.c_ulonglong, vp]
         L.gd_set_device.argtypes = [i]
         L.gd_profile_enable.argtypes = [i]
+        L.gd_debug_launch_log.argtypes = [C.POINTER(gd_launch_rec), i, i]
         L.gd_profile_read.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_longlong),
                                       C.POINTER(C.c_double), i]
         _lib = L
@@ -160,6 +166,16 @@ def profile_log(max_entries: int = 4096):
     return [(PROFILE_KINDS[kinds[i]], ms[i]) for i in range(min(n, max_entries))]
 
 
+def launch_log(reset: bool = True) -> list:
+    """Directional-pass launches since the last reset, oldest first: one dict per
+    launch group with the kernel variant that ran (path 0 persistent strip kernel,
+    1 row chain, 2 plane-step fallback; rows, warp shape, cluster size cs, ...)."""
+    n = lib().gd_debug_launch_log(None, 0, 0)
+    buf = (gd_launch_rec * max(n, 1))()
+    n = lib().gd_debug_launch_log(buf, n, 1 if reset else 0)
+    return [{f: getattr(buf[i], f) for f, _ in gd_launch_rec._fields_} for i in range(n)]
+
+
 # ---------------------------------------------------------------- host API
 def generalized_geodesic(image, soft_mask, spacing=None, lam=1.0, nu=1e10, iterations=2,
                          stats: dict | None = None) -> np.ndarray:
@@ -232,6 +248,8 @@ def scan_to_fixpoint(image, dist, spacing=None, lam=1.0, max_rounds=100, tol=1e-
     """geodist::scan_to_fixpoint, Engine::Parallel.  Returns (dist, rounds, converged, change)."""
     image = _f32(image)
     d = _f32(dist).copy()
+    if d.shape != image.shape:
+        raise InvalidArgument("scan_to_fixpoint: image/distance shape or spacing mismatch")
     g = _grid(image.shape, spacing)
     st = gd_stats()
     _check(lib().gd_scan_to_fixpoint(C.byref(g), _ptr(image), _ptr(d), lam, max_rounds, tol,
@@ -270,6 +288,25 @@ class device:
             _check(lib().gd_set_device(int(t.device.index)))
 
     @staticmethod
+    def _validate(shape, **tensors):
+        """Every tensor: a contiguous float32 CUDA tensor of exactly `shape`, on the
+        device of the first one (the library reads and writes numel() floats)."""
+        dev = None
+        for name, t in tensors.items():
+            if not getattr(t, "is_cuda", False):
+                raise InvalidArgument(f"{name}: expected a CUDA tensor")
+            if str(t.dtype) != "torch.float32":
+                raise InvalidArgument(f"{name}: expected float32, got {t.dtype}")
+            if not t.is_contiguous():
+                raise InvalidArgument(f"{name}: expected a contiguous tensor")
+            if tuple(t.shape) != tuple(shape):
+                raise InvalidArgument(f"{name}: shape {tuple(t.shape)} != {tuple(shape)}")
+            if dev is None:
+                dev = t.device
+            elif t.device != dev:
+                raise InvalidArgument(f"{name}: on {t.device}, expected {dev}")
+
+    @staticmethod
     def _stream(stream):
         if stream is not None:
             return C.c_void_p(stream)
@@ -280,8 +317,9 @@ class device:
     def generalized_geodesic(image, soft_mask, out, spacing=None, lam=1.0, nu=1e10,
                              iterations=2, batch=None, stream=None):
         """image/soft_mask/out: contiguous float32 CUDA tensors of shape [B?, (D,) H, W]."""
-        device._bind(image)
         shape = tuple(image.shape)
+        device._validate(shape, image=image, soft_mask=soft_mask, out=out)
+        device._bind(image)
         if batch:
             g = _grid(shape[1:], spacing)
         else:
@@ -296,6 +334,7 @@ class device:
     @staticmethod
     def gsf(image, soft_mask, out, spacing=None, lam=1.0, nu=1e10, iterations=2, theta=0.0,
             stream=None):
+        device._validate(tuple(image.shape), image=image, soft_mask=soft_mask, out=out)
         device._bind(image)
         g = _grid(tuple(image.shape), spacing)
         st = gd_stats()
@@ -307,6 +346,7 @@ class device:
 
     @staticmethod
     def parallel_scan(image, dist, spacing=None, lam=1.0, iterations=2, stream=None):
+        device._validate(tuple(image.shape), image=image, dist=dist)
         device._bind(image)
         g = _grid(tuple(image.shape), spacing)
         _check(lib().gd_parallel_scan(C.byref(g), C.c_void_p(image.data_ptr()),
@@ -315,6 +355,7 @@ class device:
 
     @staticmethod
     def fill_splitmix(out, seed: int, stream=None):
+        device._validate(tuple(out.shape), out=out)
         device._bind(out)
         _check(lib().gd_fill_splitmix(C.c_void_p(out.data_ptr()), out.numel(),
                                       C.c_ulonglong(seed), device._stream(stream)))

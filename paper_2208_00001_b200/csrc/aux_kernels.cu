@@ -85,13 +85,14 @@ __device__ __forceinline__ float init_value(float m, double nu) {
 // Soft-mask init fused with the input checks: one pass over image + mask.
 // `img` may be null (no exactness check wanted).  `m` and `d` views may differ
 // (the distance may live in a padded working layout).
+// `vec`: the host found every pointer 16-byte aligned (float4 path allowed).
 __global__ void init_check_kernel(VolView mv, VolView dv, const float* img, const float* mask,
-                                  float* dist, double nu, ImageCheck* out, long long n) {
+                                  float* dist, double nu, ImageCheck* out, long long n, bool vec) {
     ExpStats st;
     int bad = 0;
     const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
     const long long t0 = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-    if (dense(mv) && dense(dv) && (n & 3) == 0) {
+    if (vec && dense(mv) && dense(dv) && (n & 3) == 0) {
         const long long n4 = n >> 2;
         // Two float4 per stream in flight per thread (all loads issued first):
         // 0.37 ms at 512^3 with one, a 3-stream read/read/write copy.
@@ -131,12 +132,12 @@ __global__ void init_check_kernel(VolView mv, VolView dv, const float* img, cons
 
 // Exactness / mask-range check alone (scans that are not generalized_geodesic).
 __global__ void image_check_kernel(VolView v, const float* img, const float* mask,
-                                   ImageCheck* out, long long n) {
+                                   ImageCheck* out, long long n, bool vec) {
     ExpStats st;
     int bad = 0;
     const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
     const long long t0 = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-    if (dense(v) && (n & 3) == 0) {
+    if (vec && dense(v) && (n & 3) == 0) {
         const long long n4 = n >> 2;
         for (long long i = t0; i < n4; i += stride) {
             if (img) {
@@ -312,6 +313,8 @@ __global__ void splitmix_kernel(float* out, long long n, unsigned long long seed
     }
 }
 
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
 int sm_count() {
     static int sms = 0;
     if (!sms) {
@@ -347,7 +350,9 @@ cudaError_t launch_init_generalized(const VolView& m, const VolView& d, const fl
         check = dummy;
         img = nullptr;
     }
-    init_check_kernel<<<grid_for((n + 3) / 4, 256), 256, 0, s>>>(m, d, img, mask, dist, nu, check, n);
+    const bool vec = aligned16(mask) && aligned16(dist) && (!img || aligned16(img));
+    init_check_kernel<<<grid_for((n + 3) / 4, 256), 256, 0, s>>>(m, d, img, mask, dist, nu, check, n,
+                                                                 vec);
     return cudaGetLastError();
 }
 
@@ -374,7 +379,8 @@ cudaError_t launch_image_check(const VolView& v, const float* img, const float* 
     ImageCheck init{-1000, 1000, 0, 0, 0, 0};
     cudaError_t e = cudaMemcpyAsync(out, &init, sizeof(init), cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return e;
-    image_check_kernel<<<grid_for((n + 3) / 4, 256), 256, 0, s>>>(v, img, mask, out, n);
+    const bool vec = (!img || aligned16(img)) && (!mask || aligned16(mask));
+    image_check_kernel<<<grid_for((n + 3) / 4, 256), 256, 0, s>>>(v, img, mask, out, n, vec);
     return cudaGetLastError();
 }
 

@@ -86,6 +86,9 @@ int run(int mem, void* stream, long long n, const float* img, const float* aux, 
         bool io_in, F&& fn) {
     if (int rc = check_device()) return rc;
     if (mem == GD_MEM_DEVICE) {
+        // asynchronous: a watchdog raised by earlier work on this device is reported here
+        gdb::Status w = gdb::take_watchdog();
+        if (!w.ok()) return fail(w);
         gdb::Status s = fn(img, aux, io, static_cast<cudaStream_t>(stream));
         return s.ok() ? GD_OK : fail(s);
     }
@@ -114,7 +117,8 @@ int run(int mem, void* stream, long long n, const float* img, const float* aux, 
     if ((e = cudaMemcpyAsync(io, d_io, bytes, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
         return cuda_fail(e, "D2H result");
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "stream sync");
-    return GD_OK;
+    gdb::Status w = gdb::take_watchdog();
+    return w.ok() ? GD_OK : fail(w);
 }
 
 }  // namespace
@@ -223,6 +227,11 @@ int gd_profile_read(double* ms4, long long* count4, double* bytes4, int reset) {
 }
 
 int gd_profile_log(int* kinds, float* ms, int max) { return gdb::profile_log(kinds, ms, max); }
+
+static_assert(sizeof(gd_launch_rec) == sizeof(gdb::LaunchRec), "launch record layout");
+int gd_debug_launch_log(gd_launch_rec* out, int max, int reset) {
+    return gdb::launch_log(reinterpret_cast<gdb::LaunchRec*>(out), out ? max : 0, reset != 0);
+}
 
 int gd_fill_splitmix(float* device_out, long long n, unsigned long long seed, void* stream) {
     if (int rc = check_device()) return rc;

@@ -29,6 +29,13 @@ namespace {
 std::atomic<long long> g_launches{0};
 std::atomic<bool> g_exact_blend{false};
 
+std::mutex g_log_mu;
+std::vector<LaunchRec> g_log;
+void log_launch(const LaunchRec& r) {
+    std::lock_guard<std::mutex> lk(g_log_mu);
+    if (g_log.size() < static_cast<size_t>(kLaunchLogMax)) g_log.push_back(r);
+}
+
 // Optional per-launch CUDA-event timing, recorded on the launching stream
 // (bench.py's roofline numbers).  Off by default.
 struct Profiler {
@@ -122,6 +129,11 @@ struct StreamCtx {
 struct DeviceCtx {
     std::mutex mu;
     std::map<cudaStream_t, StreamCtx> streams;
+    // Halo watchdog word in mapped pinned host memory: the sweep kernel sets it
+    // when a neighbour wait exceeds the spin limit; the host reads it without a
+    // stream synchronisation.
+    unsigned int* err_h = nullptr;
+    unsigned int* err_d = nullptr;
 };
 
 DeviceCtx& device_ctx() {
@@ -129,6 +141,26 @@ DeviceCtx& device_ctx() {
     int dev = 0;
     cudaGetDevice(&dev);
     return ctx[dev & 63];
+}
+
+// Device pointer of this device's watchdog word (allocated on first use; null if
+// mapped host memory is unavailable, which only disables the report).
+unsigned int* watchdog_word(DeviceCtx& dc) {
+    if (!dc.err_d) {
+        void* h = nullptr;
+        if (cudaHostAlloc(&h, sizeof(unsigned int), cudaHostAllocMapped) == cudaSuccess) {
+            *static_cast<volatile unsigned int*>(h) = 0u;
+            void* d = nullptr;
+            if (cudaHostGetDevicePointer(&d, h, 0) == cudaSuccess) {
+                dc.err_h = static_cast<unsigned int*>(h);
+                dc.err_d = static_cast<unsigned int*>(d);
+            } else {
+                cudaFreeHost(h);
+            }
+        }
+        (void)cudaGetLastError();
+    }
+    return dc.err_d;
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -400,6 +432,7 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
                                  (kind == kSpatial ? 8.0 : 12.0);
             ProfScope ps(kProfSweep, bytes, s);
             GD_CK(launch_row_chain(kind, f64, p, s));
+            log_launch({axis, npass, kind, f64 ? 1 : 0, 1, 0, 0, 0, 1, 1, p.nvol, p.nvol, 0});
             g_launches += 1;
             if (st) st->kernel_launches += 1;
         }
@@ -422,6 +455,7 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
                                  (kind == kSpatial ? 8.0 : 12.0);
             ProfScope ps(kProfSweep, bytes, s);
             for (int j = 1; j <= J; ++j) GD_CK(launch_plane_step(kind, f64, p, plane(j), plane(j - 1), s));
+            log_launch({axis, npass, kind, f64 ? 1 : 0, 2, 0, 0, 0, 1, 0, p.nvol, 0, 0});
             g_launches += J;
             if (st) st->kernel_launches += J;
         }
@@ -467,6 +501,7 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
             p.ghost = sc.ghost.as<float>();
         }
         p.tag_base = sc.tag;
+        p.err = watchdog_word(device_ctx());
         sc.tag += static_cast<uint32_t>(J + 1);
         // Diagnostic cycle counters: only a -DGD_SWEEP_TRACE build writes them.
         static const bool trace_on = std::getenv("GEODIST_SWEEP_TRACE") != nullptr;
@@ -484,6 +519,8 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
             ProfScope ps(kProfSweep, bytes, s);
             GD_CK(launch_sweep(kind, f64, R, tb, tm_d, tm_i, p, s));
         }
+        log_launch({axis, npass, kind, f64 ? 1 : 0, 0, R, nwv, sweep_warp_rows(R, nwv, kind), p.cs,
+                    ntu, nvol, nvol * ntu, tb ? 1 : 0});
         if (trace_on) {
             std::vector<long long> h(trace_n);
             GD_CK(cudaMemcpyAsync(h.data(), sc.trace.p, trace_n * sizeof(long long),
@@ -834,6 +871,26 @@ Status fill_splitmix(float* out, long long n, unsigned long long seed, cudaStrea
     GD_CK(launch_splitmix(out, n, seed, s));
     ++g_launches;
     return Status::Ok();
+}
+
+Status take_watchdog() {
+    DeviceCtx& dc = device_ctx();
+    std::lock_guard<std::mutex> lk(dc.mu);
+    if (!dc.err_h) return Status::Ok();
+    volatile unsigned int* w = dc.err_h;
+    if (*w == 0u) return Status::Ok();
+    *w = 0u;
+    return {kCudaError,
+            "halo watchdog: a strip of the directional-pass kernel waited past the spin limit "
+            "for its neighbour; the results of the work enqueued since the last check are invalid"};
+}
+
+int launch_log(LaunchRec* out, int max, bool reset) {
+    std::lock_guard<std::mutex> lk(g_log_mu);
+    const int n = static_cast<int>(g_log.size());
+    for (int i = 0; i < n && i < max; ++i) out[i] = g_log[i];
+    if (reset) g_log.clear();
+    return n;
 }
 
 int profile_log(int* kinds, float* ms, int max) {

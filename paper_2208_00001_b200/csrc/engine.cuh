@@ -77,6 +77,32 @@ Status fill_splitmix(float* out, long long n, unsigned long long seed, cudaStrea
 // bench.py's gpu_launches).
 long long kernel_launch_count();
 
+// Launch log of the directional-pass kernels (tests assert which variant ran):
+// one record per sweep launch group, in launch order, capped at kLaunchLogMax.
+struct LaunchRec {
+    int axis;       // 0 z, 1 y, 2 x (x-layout)
+    int npass;      // 1 or 2 (forward+backward pair)
+    int kind;       // CostKind
+    int f64;        // f64 arithmetic path
+    int path;       // 0 persistent strip kernel, 1 row chain, 2 plane-step fallback
+    int rows;       // R: rows per strip (0 for path 1/2)
+    int nwv;        // warp columns per strip
+    int nwu;        // warp rows per strip
+    int cs;         // thread-block cluster size (1 = tagged-L2 links only)
+    int ntu;        // strips per volume
+    int nvol;       // volumes in this launch
+    int grid;       // CTAs
+    int tb;         // temporally blocked variant (halo every two planes)
+};
+constexpr int kLaunchLogMax = 4096;
+// Reads (and clears) this device's halo watchdog word: kCudaError if a sweep
+// launch enqueued since the last call gave up waiting for a neighbour.  Needs
+// no stream synchronisation (mapped host memory); a launch still running may
+// raise it later.
+Status take_watchdog();
+// Copies up to `max` records (oldest first); returns the number logged.
+int launch_log(LaunchRec* out, int max, bool reset);
+
 // Per-launch CUDA-event profiling by kernel class (on the launching stream).
 enum ProfKind : int { kProfSweep = 0, kProfTranspose = 1, kProfInit = 2, kProfOther = 3, kProfKinds = 4 };
 void profile_enable(bool on);

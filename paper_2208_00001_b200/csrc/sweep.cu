@@ -3,6 +3,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 
 #include "sweep.cuh"
@@ -13,7 +14,15 @@ namespace gdb {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr long long kSpinLimit = 1ll << 24;  // ~seconds of polling: a protocol bug traps, never hangs
+constexpr long long kSpinLimit = 1ll << 22;  // ~seconds of polling: then the watchdog word is set
+
+// Watchdog: set the word (system scope: it lives in mapped host memory).
+__device__ __forceinline__ void watchdog_raise(unsigned int* err) {
+    if (err) atomicOr_system(err, 1u);
+}
+__device__ __forceinline__ bool watchdog_raised(const unsigned int* err) {
+    return err && *reinterpret_cast<const volatile unsigned int*>(err) != 0u;
+}
 
 // Halo polls: one per step, issued at the top of the step.  Measured slower on
 // B200 at 512^3: a second poll in flight mid-step (1.48 vs 1.24 us/step: more
@@ -515,7 +524,16 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p,
                     if (TOP && l2_up) load_row(hup + k * VW, hu[k]);
                     if (BOT && l2_dn) load_row(hdn + k * VW, hd[k]);
                 }
-                if (++spins > kSpinLimit) __trap();
+                // Watchdog: after kSpinLimit polls (or once another CTA raised it,
+                // checked every 1024 polls) give up on this neighbour; the host
+                // reports the failure instead of a hang or a sticky trap.
+                ++spins;
+                const bool give_up = spins > kSpinLimit ||
+                                     ((spins & 1023) == 0 && watchdog_raised(p.err));
+                if (__any_sync(kFull, give_up)) {
+                    if (lane == 0) watchdog_raise(p.err);
+                    break;
+                }
             }
             const uint32_t rph = static_cast<uint32_t>(((j - 1) >> 1) & 1);
             if (TOP && ds_up) mbar_wait(&c.rbar[rq * 2 + 0], rph);
@@ -873,7 +891,11 @@ cudaError_t launch_one(const CUtensorMap& tm_d, const CUtensorMap& tm_i, const S
         at[1].id = cudaLaunchAttributeCooperative;
         at[1].val.cooperative = 1;
         cfg.attrs = at;
-        cfg.numAttrs = 2;
+        // Profiling only (GEODIST_SWEEP_NOCOOP=1): drop the cooperative attribute.
+        // The grid is sized to the co-resident cluster count either way; ncu's
+        // kernel replay rejects the cooperative + cluster launch (LaunchFailed).
+        static const bool nocoop = std::getenv("GEODIST_SWEEP_NOCOOP") != nullptr;
+        cfg.numAttrs = nocoop ? 1 : 2;
         return cudaLaunchKernelEx(&cfg, fn, tm_d, tm_i, p);
     }
     void* args[] = {const_cast<CUtensorMap*>(&tm_d), const_cast<CUtensorMap*>(&tm_i),

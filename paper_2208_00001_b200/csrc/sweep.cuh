@@ -78,6 +78,9 @@ struct SweepParams {
     long long* trace;         // optional per-warp cycle counters (null in production)
     float* ghost;             // TB: forward ghost rows, [cta][TOP|BOT][n1/2+1][nwv*128]
     const float* image;       // plane-step fallback: intensities (same layout as dist)
+    unsigned int* err;        // watchdog word (mapped host memory): a halo wait that exceeds
+                              // the spin limit sets it and every later wait gives up, so a
+                              // protocol failure ends the launch and is reported, never hangs
     int debug_flags;          // experiments only (GD_SWEEP_TRACE builds): 1 no spin, 2 no halo stores, 4 no halo loads
     // Neighbour coefficients indexed (du+1)*3 + (dv+1).
     double rho[9];

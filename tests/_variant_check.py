@@ -1,8 +1,13 @@
 """Parity of one kernel variant (selected by environment, read once per process).
 
 Run by tests/test_variants_gpu.py in a subprocess:
-    GEODIST_SWEEP_TB=1 python tests/_variant_check.py
-Exits 1 with a message on the first mismatch against the C oracle.
+    GEODIST_SWEEP_TB=1 GD_EXPECT="any:tb=1" python tests/_variant_check.py
+Exits 1 with a message on the first mismatch against the C oracle, or when the
+launch log (gd_debug_launch_log) shows the variant the environment asked for
+never ran.  GD_EXPECT: ';'-separated clauses "any:key=v" (some launch has it; "any:k1=v1,k2=v2" for
+a conjunction), "all:key=v" (every launch of the persistent strip kernel has it), "allp:key=v"
+(every launch of any path), "none:key=v" (no launch has it); keys are the
+gd_launch_rec fields (path, rows, nwu, cs, tb, ...).
 """
 import os
 import sys
@@ -20,13 +25,37 @@ CASES = [
     ((20, 70, 132), (1.0, 1.0, 2.5)),
     ((9, 130, 260), (1.0, 1.0, 1.0)),
     ((24, 17, 520), (2.0, 1.0, 1.0)),
+    # strip counts divisible by 8 on every axis pair, so clusters of 2/4/8 form:
+    # z plane 288x300 (72 strips, 3 warp columns), y/x planes 30 rows (8 strips,
+    # partial last strip); z plane 62x100 (16 strips, 1 warp column)
+    ((30, 288, 300), (1.0, 1.0, 2.5)),
+    ((30, 62, 100), (1.0, 1.3, 1.0)),
     ((45, 300), (1.0, 1.5)),  # 2D: row-chain kernel (or the strip kernel's R = 1 shape)
     ((7, 130), (1.0, 1.0)),
 ]
 
 
+def check_expectations(log, spec):
+    persist = [r for r in log if r["path"] == 0]
+    for clause in filter(None, spec.split(";")):
+        mode, kv = clause.split(":", 1)
+        want = {k: int(v) for k, v in (x.split("=") for x in kv.split(","))}
+        pool = persist if mode == "all" else log
+        hits = [r for r in pool if all(r[k] == v for k, v in want.items())]
+        if mode == "any" and not hits:
+            return f"no launch with {kv}"
+        if mode in ("all", "allp") and (not pool or len(hits) != len(pool)):
+            bad = [r for r in pool if r not in hits][:3]
+            return f"launches without {kv}: {bad}"
+        if mode == "none" and hits:
+            return f"launches with {kv}: {hits[:3]}"
+    return None
+
+
 def main():
     o = COracle()
+    gd.launch_log(reset=True)
+    log = []
     for shape, sp in CASES:
         for lam in (0.0, 0.7, 1.0):
             rng = np.random.default_rng(hash((shape, lam)) % 2**32)
@@ -51,7 +80,12 @@ def main():
                     if not ok:
                         print(f"mismatch pass shape={shape} lam={lam} axis={axis} o={orient}")
                         return 1
-    print("ok")
+            log += gd.launch_log(reset=True)
+    err = check_expectations(log, os.environ.get("GD_EXPECT", ""))
+    if err:
+        print("variant not exercised:", err)
+        return 1
+    print(f"ok ({len(log)} launches)")
     return 0
 
 

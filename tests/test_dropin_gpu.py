@@ -1,0 +1,49 @@
+"""The reference's OWN tests run against the drop-in on the B200.
+
+oracle/Makefile (target dropin-tests, built by __graft_entry__.build() where
+/root/reference exists) compiles the reference's unit tests
+(test_{grid,metric,scan_parallel,transforms}.cpp, 44 cases) and its acceptance
+suite (acceptance_main.cpp, A1-A9) unchanged, with include/geodist first on the
+include path, linked against paper_2208_00001_b200/lib/libgeodist_b200.so.
+Here the prebuilt binaries run on the GPU: every case passes except those that
+call the reference's CPU-only engines (oracle/dropin_expected_fail.txt; A1/A2
+run Engine::Serial, A6 needs the reference CLI), which the drop-in rejects by
+design.  Replaces: /root/reference/proj/tests/CMakeLists.txt:1-25 (unit_tests,
+acceptance_suite)."""
+import os
+import subprocess
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BIN = os.path.join(ROOT, "oracle", "_ref")
+
+
+def _run(name, env=None):
+    path = os.path.join(BIN, name)
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not built (make -C oracle dropin-tests, needs /root/reference)")
+    e = dict(os.environ, **(env or {}))
+    return subprocess.run([path], capture_output=True, text=True, timeout=900, env=e)
+
+
+def test_reference_unit_tests_on_dropin():
+    r = _run("dropin_unit_tests",
+             {"GD_EXPECTED_FAIL": os.path.join(ROOT, "oracle", "dropin_expected_fail.txt")})
+    out = r.stdout
+    assert r.returncode == 0, out[-4000:] + r.stderr[-2000:]
+    summary = [ln for ln in out.splitlines() if ln.startswith("== ")][-1]
+    assert "0 failed" in summary and "2 expected failures" in summary, summary
+    assert "44 test cases: 42 passed" in summary, summary
+
+
+def test_reference_acceptance_on_dropin():
+    r = _run("dropin_acceptance")
+    out = r.stdout
+    assert r.returncode == 0, out[-4000:] + r.stderr[-2000:]
+    lines = out.splitlines()
+    for crit in ("A1p", "A3", "A4", "A5", "A7", "A9"):
+        assert any(ln.startswith(f"{crit} ") and ": PASS" in ln for ln in lines), (crit, out)
+    assert "dropin acceptance: 0 unexpected failure(s)" in out

@@ -172,6 +172,34 @@ def test_row_chain_batched_2d(gd, oracle, lam):
         _check(g[b], oracle.generalized_geodesic(imgs[b], masks[b], sp, lam, 1e10, 2), lam)
 
 
+@pytest.mark.parametrize("lam,cs", [(1.0, 4), (0.0, 2)])
+@pytest.mark.parametrize("shape", [(12, 256, 512), (10, 288, 400)], ids=["full_w512", "partial_w400"])
+def test_default_cluster_instances(gd, oracle, shape, lam, cs):
+    """The production clustered sweeps behind the 512^3 headline: planes of >= 64
+    strips of 4 rows and 4 warp columns take DSMEM halo links in clusters of 4
+    (intensity) / 2 (spatial) by default.  The launch log proves the z pair ran
+    clustered (64 / 72 strips; full and partial last warp column); the whole
+    transform and every single pass are bit-exact against the oracle."""
+    rng = np.random.default_rng(41)
+    img = dyadic_image(rng, shape)
+    m = point_mask(shape)
+    sp = (1.0, 1.0, 2.5)
+    gd.launch_log(reset=True)
+    g = gd.generalized_geodesic(img, m, sp, lam, 1e10, 2)
+    log = gd.launch_log(reset=True)
+    zl = [r for r in log if r["axis"] == 0]
+    assert zl and all(r["cs"] == cs and r["nwv"] == 4 and r["rows"] == 4 and r["path"] == 0
+                      for r in zl), zl
+    assert all(r["cs"] == 1 for r in log if r["axis"] != 0)  # 3-strip planes: L2 links
+    r = oracle.generalized_geodesic(img, m, sp, lam, 1e10, 2)
+    assert bitwise_equal(g, r), parity(g, r)
+    d0 = seed_init(rng, shape, 5)
+    for o in (1, -1):
+        assert bitwise_equal(gd.directional_pass(d0, img, 0, o, sp, lam),
+                             oracle.directional_pass(d0, img, 0, o, sp, lam))
+    assert all(r["cs"] == cs for r in gd.launch_log(reset=True) if r["axis"] == 0)
+
+
 @pytest.mark.parametrize("shape", [(3, 6, 2100), (3, 1300, 600)],
                          ids=["wider_than_2048", "more_strips_than_sms"])
 def test_large_planes_plane_step(gd, oracle, shape):

@@ -19,6 +19,7 @@ ap.add_argument("--spacing", default="1,1,2.5")
 ap.add_argument("--iters", type=int, default=4)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--batch", type=int, default=1)
+ap.add_argument("--gsf", action="store_true")
 a = ap.parse_args()
 shape = tuple(int(x) for x in a.shape.split(","))
 full = ((a.batch,) + shape) if a.batch > 1 else shape
@@ -29,7 +30,12 @@ mask = torch.ones(full, dtype=torch.float32, device="cuda")
 mask[tuple(s // 2 for s in full)] = 0.0
 out = torch.empty_like(img)
 for _ in range(a.reps):
-    gd.device.generalized_geodesic(img, mask, out, spacing, a.lam, 1e10, a.iters,
-                                   batch=a.batch if a.batch > 1 else None)
+    if a.gsf:
+        gd.device.gsf(img, mask, out, spacing, a.lam, 1e10, a.iters, 2.0)
+    else:
+        gd.device.generalized_geodesic(img, mask, out, spacing, a.lam, 1e10, a.iters,
+                                       batch=a.batch if a.batch > 1 else None)
 torch.cuda.synchronize()
 print("ok", float(out.max().item()))
+for r in gd.launch_log()[:12]:
+    print("launch", r)
