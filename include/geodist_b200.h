@@ -13,9 +13,17 @@
  * through the device and synchronises before returning, like the reference's
  * blocking calls) or GD_MEM_DEVICE (pointers are device memory on the current
  * CUDA device; work is enqueued on `stream` (a cudaStream_t, NULL = legacy
- * default stream).  Calls that must read a device-side result to decide
- * control flow — the mask-range / image-exactness check, GSF's empty-complement
- * test, fixpoint convergence — synchronise `stream`).
+ * default stream) and the call returns without blocking).  Decisions that
+ * depend on the data are taken on the device: the soft-mask range check, the
+ * f32 / f64 choice for lambda = 1 and GSF's empty-complement skip set a gate
+ * word the transform's kernels test.  Errors found that way (mask values
+ * outside [0, 1]; the halo watchdog) are DEFERRED: they are returned by the
+ * next call on the device or by gd_synchronize(), like CUDA's asynchronous
+ * errors; host-memory calls check them before copying results back, so the
+ * caller's output stays untouched on error as with the reference.  Only
+ * scan_to_fixpoint (a host-side convergence loop, one sync per round) and
+ * gd_gsf with a non-NULL `stats` (complement_empty needs the device count)
+ * synchronise a device-memory call.
  *
  * There is no CPU fallback: if no CUDA device is usable every call returns
  * GD_CUDA_ERROR.
@@ -129,6 +137,11 @@ typedef struct gd_launch_rec {
     int tb;    /* temporally blocked variant (halo exchanged every two planes) */
 } gd_launch_rec;
 int gd_debug_launch_log(gd_launch_rec* out, int max, int reset);
+
+/* Waits for `stream` and returns any deferred error of the work enqueued on
+ * this device (GD_INVALID_ARGUMENT for a soft mask outside [0, 1],
+ * GD_CUDA_ERROR for a CUDA error or the halo watchdog). */
+int gd_synchronize(void* stream);
 
 /* Utilities. */
 /* Selects the CUDA device for this thread's subsequent calls (the library

@@ -90,6 +90,7 @@ def lib():
         L.gd_kernel_launches.restype = C.c_longlong
         L.gd_fill_splitmix.argtypes = [fp, C.c_longlong, C.c_ulonglong, vp]
         L.gd_set_device.argtypes = [i]
+        L.gd_synchronize.argtypes = [vp]
         L.gd_profile_enable.argtypes = [i]
         L.gd_debug_launch_log.argtypes = [C.POINTER(gd_launch_rec), i, i]
         L.gd_profile_read.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_longlong),
@@ -281,6 +282,12 @@ class device:
     @staticmethod
     def set_device(index: int) -> None:
         _check(lib().gd_set_device(int(index)))
+
+    @staticmethod
+    def synchronize(stream=None) -> None:
+        """Waits for the stream and raises any deferred error of the asynchronous
+        calls (InvalidArgument for a soft mask outside [0, 1])."""
+        _check(lib().gd_synchronize(device._stream(stream)))
 
     @staticmethod
     def _bind(t) -> None:

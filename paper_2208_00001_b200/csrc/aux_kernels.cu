@@ -9,6 +9,7 @@
 #include <cstdint>
 
 #include "aux_kernels.cuh"
+#include "sweep.cuh"
 
 namespace gdb {
 
@@ -275,12 +276,41 @@ __global__ void gsf_dilate_kernel(VolView v, const float* dist, float* out, doub
 
 // erode epilogue: out = [f64(D) > theta]
 __global__ void gsf_erode_kernel(VolView v, const float* dist, VolView o, float* out, double theta,
-                                 long long n) {
+                                 long long n, const int* gate) {
+    if (gate && (*gate & kGateSkip)) return;  // empty complement: out keeps K
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
         const float d = dist[vox_offset(v, i)];
         out[vox_offset(o, i)] = static_cast<double>(d) > theta ? 1.0f : 0.0f;
     }
+}
+
+__global__ void reset_check_kernel(ImageCheck* c) {
+    *c = ImageCheck{-1000, 1000, 0, 0, 0, 0};
+}
+
+// Turns the fused init/check statistics into the gate word the transform's
+// kernels test (sweep.cuh GateBits): mask range, the f32/f64 choice for
+// lambda = 1 (every I_p - I_q exact in f32 when all values are multiples of
+// 2^tmin below 2^(emax+1) with emax - tmin <= 23, 22 with mixed signs), GSF's
+// empty-complement skip.  A bad mask also raises the deferred-error bit of the
+// device's status word (mapped host memory).
+__global__ void decide_kernel(const ImageCheck* chk, int check_exact,
+                              const unsigned long long* skip_if_zero, int* gate,
+                              unsigned int* status) {
+    const ImageCheck h = *chk;
+    int g = 0;
+    if (h.bad_mask) g |= kGateMaskBad;
+    if (check_exact) {
+        bool exact;
+        if (h.nonfinite) exact = false;
+        else if (h.emax < -999) exact = true;  // all zeros
+        else exact = (h.emax - h.tmin) <= ((h.pos && h.neg) ? 22 : 23);
+        if (!exact) g |= kGateF64;
+    }
+    if (skip_if_zero && *skip_if_zero == 0ull) g |= kGateSkip;
+    *gate = g;
+    if ((g & kGateMaskBad) && status) atomicOr_system(status, kStatusMaskBad);
 }
 
 // Fixpoint change: max over voxels of f64(before) - f64(after) (scan_parallel.cpp:386-392).
@@ -339,8 +369,8 @@ cudaError_t launch_init_generalized(const VolView& m, const VolView& d, const fl
                                     cudaStream_t s) {
     const long long n = m.count();
     if (check) {
-        ImageCheck init{-1000, 1000, 0, 0, 0, 0};
-        cudaError_t e = cudaMemcpyAsync(check, &init, sizeof(init), cudaMemcpyHostToDevice, s);
+        reset_check_kernel<<<1, 1, 0, s>>>(check);
+        cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
     // a scratch check target when the caller does not want one
@@ -376,8 +406,8 @@ cudaError_t launch_transpose(const VolView& src_v, const VolView& dst_v, const f
 cudaError_t launch_image_check(const VolView& v, const float* img, const float* mask,
                                ImageCheck* out, cudaStream_t s) {
     const long long n = v.count();
-    ImageCheck init{-1000, 1000, 0, 0, 0, 0};
-    cudaError_t e = cudaMemcpyAsync(out, &init, sizeof(init), cudaMemcpyHostToDevice, s);
+    reset_check_kernel<<<1, 1, 0, s>>>(out);
+    cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const bool vec = (!img || aligned16(img)) && (!mask || aligned16(mask));
     image_check_kernel<<<grid_for((n + 3) / 4, 256), 256, 0, s>>>(v, img, mask, out, n, vec);
@@ -399,9 +429,16 @@ cudaError_t launch_gsf_dilate(const VolView& v, const float* dist, float* out, d
 }
 
 cudaError_t launch_gsf_erode(const VolView& v, const float* dist, const VolView& o, float* out,
-                             double theta, cudaStream_t s) {
+                             double theta, const int* gate, cudaStream_t s) {
     const long long n = v.count();
-    gsf_erode_kernel<<<grid_for(n, 256), 256, 0, s>>>(v, dist, o, out, theta, n);
+    gsf_erode_kernel<<<grid_for(n, 256), 256, 0, s>>>(v, dist, o, out, theta, n, gate);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_decide(const ImageCheck* chk, bool check_exact,
+                          const unsigned long long* skip_if_zero, int* gate, unsigned int* status,
+                          cudaStream_t s) {
+    decide_kernel<<<1, 1, 0, s>>>(chk, check_exact ? 1 : 0, skip_if_zero, gate, status);
     return cudaGetLastError();
 }
 

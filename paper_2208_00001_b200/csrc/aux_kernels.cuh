@@ -34,7 +34,14 @@ cudaError_t launch_gsf_sources(const VolView& v, const float* mask, const VolVie
 cudaError_t launch_gsf_dilate(const VolView& v, const float* dist, float* out, double theta,
                               unsigned long long* n_complement, cudaStream_t s);
 cudaError_t launch_gsf_erode(const VolView& v, const float* dist, const VolView& o, float* out,
-                             double theta, cudaStream_t s);
+                             double theta, const int* gate, cudaStream_t s);
+// Deferred-error bits of the per-device status word (mapped host memory).
+constexpr unsigned int kStatusWatchdog = 1u;  // a halo wait hit the spin limit
+constexpr unsigned int kStatusMaskBad = 2u;   // a soft mask outside [0, 1]
+// One thread: ImageCheck (+ optional GSF count) -> gate word (sweep.cuh GateBits).
+cudaError_t launch_decide(const ImageCheck* chk, bool check_exact,
+                          const unsigned long long* skip_if_zero, int* gate, unsigned int* status,
+                          cudaStream_t s);
 cudaError_t launch_max_change(const VolView& v, const float* before, const float* after,
                               unsigned long long* out, cudaStream_t s);
 cudaError_t launch_splitmix(float* out, long long n, unsigned long long seed, cudaStream_t s);

@@ -86,8 +86,9 @@ int run(int mem, void* stream, long long n, const float* img, const float* aux, 
         bool io_in, F&& fn) {
     if (int rc = check_device()) return rc;
     if (mem == GD_MEM_DEVICE) {
-        // asynchronous: a watchdog raised by earlier work on this device is reported here
-        gdb::Status w = gdb::take_watchdog();
+        // asynchronous: a deferred error of earlier work on this device (halo
+        // watchdog, soft mask out of range) is reported here, before enqueuing more
+        gdb::Status w = gdb::take_deferred();
         if (!w.ok()) return fail(w);
         gdb::Status s = fn(img, aux, io, static_cast<cudaStream_t>(stream));
         return s.ok() ? GD_OK : fail(s);
@@ -114,11 +115,15 @@ int run(int mem, void* stream, long long n, const float* img, const float* aux, 
         cudaStreamSynchronize(s);
         return fail(st);
     }
+    // The reference validates before computing and leaves the caller's output
+    // untouched on error: check the device's deferred-error word before the D2H.
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "stream sync");
+    gdb::Status w = gdb::take_deferred();
+    if (!w.ok()) return fail(w);
     if ((e = cudaMemcpyAsync(io, d_io, bytes, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
         return cuda_fail(e, "D2H result");
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "stream sync");
-    gdb::Status w = gdb::take_watchdog();
-    return w.ok() ? GD_OK : fail(w);
+    return GD_OK;
 }
 
 }  // namespace
@@ -166,9 +171,13 @@ int gd_gsf(const gd_grid* grid, const float* image, const float* soft_mask, doub
     if (int rc = grid_of(grid, &g)) return rc;
     if (!image || !soft_mask || !out) return fail(GD_INVALID_ARGUMENT, "null buffer");
     gdb::ScanStats st;
+    // complement_empty / rounds need the device's count: a device-memory call
+    // synchronises only when the caller asks for stats
+    const bool sync_stats = mem != GD_MEM_DEVICE || stats != nullptr;
     int rc = run(mem, stream, g.voxels(), image, soft_mask, out, false,
                  [&](const float* i, const float* m, float* o, cudaStream_t s) {
-                     return gdb::gsf(g, i, m, o, lambda, nu, iterations, theta, s, &st);
+                     return gdb::gsf(g, i, m, o, lambda, nu, iterations, theta, s, &st,
+                                     sync_stats);
                  });
     fill_stats(stats, st);
     return rc;
@@ -208,6 +217,14 @@ int gd_scan_to_fixpoint(const gd_grid* grid, const float* image, float* dist, do
                  });
     fill_stats(stats, st);
     return rc;
+}
+
+int gd_synchronize(void* stream) {
+    if (int rc = check_device()) return rc;
+    cudaError_t e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "stream sync");
+    gdb::Status w = gdb::take_deferred();
+    return w.ok() ? GD_OK : fail(w);
 }
 
 int gd_set_device(int device) {

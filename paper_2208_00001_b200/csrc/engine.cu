@@ -230,39 +230,31 @@ int cost_kind(double lambda) {
     return kBlend;
 }
 
-struct Prepared {
-    bool exact_diff = true;  // every |I_p - I_q| exact in f32
-    bool mask_ok = true;
+// Device-side decision for one transform (the asynchronous path): the gate
+// word the transform's kernels test, written by decide_kernel after the fused
+// init/check (or the image check) -- no host synchronisation.
+struct Gate {
+    const int* word = nullptr;  // null: ungated (nothing to decide)
+    bool dual = false;          // lambda = 1: launch the f32 and the f64 sweep, each gated
 };
 
-// Reads back an ImageCheck (synchronising the stream) and interprets it.
-Status read_check(const ImageCheck* dev, cudaStream_t s, Prepared* out) {
-    ImageCheck h;
-    GD_CK(cudaMemcpyAsync(&h, dev, sizeof(h), cudaMemcpyDeviceToHost, s));
-    GD_CK(cudaStreamSynchronize(s));
-    out->mask_ok = h.bad_mask == 0;
-    if (h.nonfinite) {
-        out->exact_diff = false;
-    } else if (h.emax < -999) {
-        out->exact_diff = true;  // all zeros
-    } else {
-        const int limit = (h.pos && h.neg) ? 22 : 23;
-        out->exact_diff = (h.emax - h.tmin) <= limit;
-    }
-    return Status::Ok();
-}
+int* gate_word(StreamCtx& sc) { return reinterpret_cast<int*>(sc.small.as<char>() + 64); }
 
-Status check_inputs(StreamCtx& sc, const Work& w, const float* mask, bool want_img,
-                    cudaStream_t s, Prepared* out) {
+// Image-exactness check (lambda = 1 scans that do not start from a soft mask:
+// directional_pass, parallel_scan, scan_to_fixpoint) -> gate word.
+Status check_inputs(StreamCtx& sc, const Work& w, cudaStream_t s, Gate* gate) {
     GD_ST(sc.small.ensure(256));
     ImageCheck* dev = sc.small.as<ImageCheck>();
     VolView v = w.canon();
     {
-        ProfScope ps(kProfOther, 4.0 * w.B * w.g.voxels() * ((want_img ? 1 : 0) + (mask ? 1 : 0)), s);
-        GD_CK(launch_image_check(v, want_img ? w.img : nullptr, mask, dev, s));
+        ProfScope ps(kProfOther, 4.0 * w.B * w.g.voxels(), s);
+        GD_CK(launch_image_check(v, w.img, nullptr, dev, s));
     }
-    ++g_launches;
-    return read_check(dev, s, out);
+    GD_CK(launch_decide(dev, true, nullptr, gate_word(sc), watchdog_word(device_ctx()), s));
+    g_launches += 3;
+    gate->word = gate_word(sc);
+    gate->dual = true;
+    return Status::Ok();
 }
 
 Status ensure_x_layout(StreamCtx& sc, Work& w, bool need_img, cudaStream_t s) {
@@ -285,7 +277,8 @@ Status ensure_x_layout(StreamCtx& sc, Work& w, bool need_img, cudaStream_t s) {
 // One launch group of the persistent sweep kernel: `npass` passes along
 // `axis` (canonical 0/1; 2 = the x axis in the [b][x][z][y] layout).
 Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int npass,
-                 double lambda, bool f64, cudaStream_t s, ScanStats* st) {
+                 double lambda, bool f64, const int* gate, int gate_want, cudaStream_t s,
+                 ScanStats* st) {
     const GridDesc& g = w.g;
     int ns, nu, nv, sweep_dim;
     long long ss, su, vol;
@@ -404,6 +397,9 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
     p.cs = cs;
     p.lambda = lambda;
     p.lambda_f = static_cast<float>(lambda);
+    p.gate = gate;
+    p.gate_mask = kGateMaskBad | kGateF64 | kGateSkip;
+    p.gate_want = gate_want;
     for (int du = -1; du <= 1; ++du)
         for (int dv = -1; dv <= 1; ++dv) {
             int dz, dy, dx;
@@ -553,8 +549,20 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
     return Status::Ok();
 }
 
+// One launch group per pair, or -- lambda = 1 under a device-side gate -- the
+// f32 and the f64 instance back to back, each leaving at once unless the gate
+// selects it (a skipped launch costs a few microseconds; no host sync).
+Status sweep_gated(StreamCtx& sc, const Work& w, int axis, int first_orient, int npass,
+                   double lambda, bool f64, const Gate& gate, cudaStream_t s, ScanStats* st) {
+    if (!gate.word) return run_sweep(sc, w, axis, first_orient, npass, lambda, f64, nullptr, 0, s, st);
+    if (!gate.dual)
+        return run_sweep(sc, w, axis, first_orient, npass, lambda, f64, gate.word, 0, s, st);
+    GD_ST(run_sweep(sc, w, axis, first_orient, npass, lambda, false, gate.word, 0, s, st));
+    return run_sweep(sc, w, axis, first_orient, npass, lambda, true, gate.word, kGateF64, s, st);
+}
+
 Status x_pair(StreamCtx& sc, Work& w, int first_orient, int npass, double lambda, bool f64,
-              cudaStream_t s, ScanStats* st) {
+              const Gate& gate, cudaStream_t s, ScanStats* st) {
     GD_ST(ensure_x_layout(sc, w, lambda != 0.0, s));
     const double tb = 8.0 * w.B * w.g.voxels();
     {
@@ -562,7 +570,7 @@ Status x_pair(StreamCtx& sc, Work& w, int first_orient, int npass, double lambda
         GD_CK(launch_transpose(w.canon(), w.trans(), w.dist, w.dT, true, s));
     }
     ++g_launches;
-    GD_ST(run_sweep(sc, w, 2, first_orient, npass, lambda, f64, s, st));
+    GD_ST(sweep_gated(sc, w, 2, first_orient, npass, lambda, f64, gate, s, st));
     {
         ProfScope ps(kProfTranspose, tb, s);
         GD_CK(launch_transpose(w.trans(), w.canon(), w.dT, w.dist, false, s));
@@ -571,19 +579,17 @@ Status x_pair(StreamCtx& sc, Work& w, int first_orient, int npass, double lambda
     return Status::Ok();
 }
 
-bool pick_f64(int kind, const Prepared& prep) {
-    if (kind == kIntensity) return !prep.exact_diff;
-    if (kind == kBlend) return g_exact_blend.load();
-    return false;
-}
+// f64 arithmetic for blend (exact mode); lambda = 1 decides on the device.
+bool blend_f64(int kind) { return kind == kBlend && g_exact_blend.load(); }
 
 // parallel_scan_inplace: for it: FB BF (3D) TB BT LR RL  (metric.cpp:35-44)
-Status scan_work(StreamCtx& sc, Work& w, double lambda, int iterations, bool f64,
+Status scan_work(StreamCtx& sc, Work& w, double lambda, int iterations, const Gate& gate,
                  cudaStream_t s, ScanStats* st) {
+    const bool f64 = blend_f64(cost_kind(lambda));
     for (int it = 0; it < iterations; ++it) {
-        if (w.g.ndim == 3) GD_ST(run_sweep(sc, w, 0, +1, 2, lambda, f64, s, st));
-        GD_ST(run_sweep(sc, w, 1, +1, 2, lambda, f64, s, st));
-        if (w.g.W >= 2) GD_ST(x_pair(sc, w, +1, 2, lambda, f64, s, st));
+        if (w.g.ndim == 3) GD_ST(sweep_gated(sc, w, 0, +1, 2, lambda, f64, gate, s, st));
+        GD_ST(sweep_gated(sc, w, 1, +1, 2, lambda, f64, gate, s, st));
+        if (w.g.W >= 2) GD_ST(x_pair(sc, w, +1, 2, lambda, f64, gate, s, st));
     }
     if (st) st->rounds += iterations;
     return Status::Ok();
@@ -641,15 +647,19 @@ Status validate_params(double lambda, double nu, int iterations) {
     return Status::Ok();
 }
 
+// generalized_geodesic on bound device buffers, fully asynchronous: the fused
+// init/check kernel and decide_kernel set the gate word; a bad mask closes it
+// (nothing runs; the error is reported through the device's status word).
+// skip_if_zero (GSF erode): the whole transform is gated off when *skip_if_zero == 0.
 Status generalized_locked(StreamCtx& sc, const GridDesc& g, int B, const float* img,
                           const float* mask, float* out, double lambda, double nu, int iterations,
-                          cudaStream_t s, ScanStats* st) {
+                          cudaStream_t s, ScanStats* st,
+                          const unsigned long long* skip_if_zero = nullptr) {
     GD_ST(validate_params(lambda, nu, iterations));
     Work w;
     bool padded = false;
     GD_ST(bind(sc, w, g, B, img, out, false, s, &padded));
     const int kind = cost_kind(lambda);
-    Prepared prep;
     // One pass over the caller's (dense) image + mask: soft-mask init into the
     // working distance, mask-range check, image-exactness statistics.
     VolView mv;
@@ -663,11 +673,12 @@ Status generalized_locked(StreamCtx& sc, const GridDesc& g, int B, const float* 
         GD_CK(launch_init_generalized(mv, w.canon(), mask, w.dist, nu, chk,
                                       want_img ? img : nullptr, s));
     }
-    ++g_launches;
-    GD_ST(read_check(chk, s, &prep));
-    if (!prep.mask_ok)
-        return Status::Invalid("generalized_geodesic: mask values must lie in [0, 1]");
-    GD_ST(scan_work(sc, w, lambda, iterations, pick_f64(kind, prep), s, st));
+    GD_CK(launch_decide(chk, want_img, skip_if_zero, gate_word(sc), watchdog_word(device_ctx()), s));
+    g_launches += 3;
+    Gate gate;
+    gate.word = gate_word(sc);
+    gate.dual = want_img;
+    GD_ST(scan_work(sc, w, lambda, iterations, gate, s, st));
     if (padded) GD_ST(unbind(w, out, s));
     return Status::Ok();
 }
@@ -745,13 +756,13 @@ Status directional_pass(const GridDesc& g, int B, const float* img, float* dist,
     bool padded = false;
     GD_ST(bind(sc, w, g, B, img, dist, true, s, &padded));
     const int kind = cost_kind(lambda);
-    Prepared prep;
-    if (kind == kIntensity) GD_ST(check_inputs(sc, w, nullptr, true, s, &prep));
-    const bool f64 = pick_f64(kind, prep);
+    Gate gate;
+    if (kind == kIntensity) GD_ST(check_inputs(sc, w, s, &gate));
+    const bool f64 = blend_f64(kind);
     if (axis == 2) {
-        if (g.W >= 2) GD_ST(x_pair(sc, w, orientation, 1, lambda, f64, s, st));
+        if (g.W >= 2) GD_ST(x_pair(sc, w, orientation, 1, lambda, f64, gate, s, st));
     } else {
-        GD_ST(run_sweep(sc, w, axis, orientation, 1, lambda, f64, s, st));
+        GD_ST(sweep_gated(sc, w, axis, orientation, 1, lambda, f64, gate, s, st));
     }
     if (padded) GD_ST(unbind(w, dist, s));
     return Status::Ok();
@@ -766,10 +777,9 @@ Status parallel_scan(const GridDesc& g, int B, const float* img, float* dist, do
     Work w;
     bool padded = false;
     GD_ST(bind(sc, w, g, B, img, dist, true, s, &padded));
-    const int kind = cost_kind(lambda);
-    Prepared prep;
-    if (kind == kIntensity) GD_ST(check_inputs(sc, w, nullptr, true, s, &prep));
-    GD_ST(scan_work(sc, w, lambda, iterations, pick_f64(kind, prep), s, st));
+    Gate gate;
+    if (cost_kind(lambda) == kIntensity) GD_ST(check_inputs(sc, w, s, &gate));
+    GD_ST(scan_work(sc, w, lambda, iterations, gate, s, st));
     if (padded) GD_ST(unbind(w, dist, s));
     return Status::Ok();
 }
@@ -784,7 +794,8 @@ Status generalized_geodesic(const GridDesc& g, int B, const float* img, const fl
 }
 
 Status gsf(const GridDesc& g, const float* img, const float* mask, float* out, double lambda,
-           double nu, int iterations, double theta, cudaStream_t s, ScanStats* st) {
+           double nu, int iterations, double theta, cudaStream_t s, ScanStats* st,
+           bool sync_stats) {
     GD_ST(validate_params(lambda, nu, iterations));
     if (!(theta >= 0.0)) return Status::Invalid("theta must be >= 0, got " + std::to_string(theta));
     DeviceCtx& dc = device_ctx();
@@ -806,17 +817,22 @@ Status gsf(const GridDesc& g, const float* img, const float* mask, float* out, d
     GD_CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), s));
     GD_CK(launch_gsf_dilate(v, out, out, theta, cnt, s));
     ++g_launches;
-    unsigned long long n_src = 0;
-    GD_CK(cudaMemcpyAsync(&n_src, cnt, sizeof(n_src), cudaMemcpyDeviceToHost, s));
-    GD_CK(cudaStreamSynchronize(s));
-    // geodesic_erode (transforms.cpp:204-229)
-    if (n_src == 0) {
-        if (st) st->complement_empty = true;
-        return Status::Ok();  // out already holds K = threshold(dilated)
-    }
-    GD_ST(generalized_locked(sc, g, 1, img, out, tmp, lambda, nu, iterations, s, st));
-    GD_CK(launch_gsf_erode(v, tmp, v, out, theta, s));
+    // geodesic_erode (transforms.cpp:204-229): gated on the device by the
+    // complement count -- when it is 0 every erode kernel leaves at once and out
+    // keeps K = threshold(dilated), as the reference returns `kept`.
+    GD_ST(generalized_locked(sc, g, 1, img, out, tmp, lambda, nu, iterations, s, st, cnt));
+    GD_CK(launch_gsf_erode(v, tmp, v, out, theta, gate_word(sc), s));
     ++g_launches;
+    if (sync_stats && st) {
+        // TransformStats::complement_empty (and the erode's rounds) need the count
+        unsigned long long n_src = 0;
+        GD_CK(cudaMemcpyAsync(&n_src, cnt, sizeof(n_src), cudaMemcpyDeviceToHost, s));
+        GD_CK(cudaStreamSynchronize(s));
+        if (n_src == 0) {
+            st->complement_empty = true;
+            st->rounds -= iterations;
+        }
+    }
     return Status::Ok();
 }
 
@@ -832,10 +848,8 @@ Status scan_to_fixpoint(const GridDesc& g, const float* img, float* dist, double
     Work w;
     bool padded = false;
     GD_ST(bind(sc, w, g, 1, img, dist, true, s, &padded));
-    const int kind = cost_kind(lambda);
-    Prepared prep;
-    if (kind == kIntensity) GD_ST(check_inputs(sc, w, nullptr, true, s, &prep));
-    const bool f64 = pick_f64(kind, prep);
+    Gate gate;
+    if (cost_kind(lambda) == kIntensity) GD_ST(check_inputs(sc, w, s, &gate));
     const size_t bytes = static_cast<size_t>(w.vol) * sizeof(float);
     GD_ST(sc.tmp.ensure(bytes));
     GD_ST(sc.small.ensure(256));
@@ -845,9 +859,11 @@ Status scan_to_fixpoint(const GridDesc& g, const float* img, float* dist, double
     stp->converged = false;
     int rounds = 0;
     double last = 0.0;
+    // The convergence test is a host decision per round (scan_parallel.cpp:376-395):
+    // this entry synchronises once per round.
     while (rounds < max_rounds) {
         GD_CK(cudaMemcpyAsync(sc.tmp.p, w.dist, bytes, cudaMemcpyDeviceToDevice, s));
-        GD_ST(scan_work(sc, w, lambda, 1, f64, s, nullptr));
+        GD_ST(scan_work(sc, w, lambda, 1, gate, s, nullptr));
         ++rounds;
         GD_CK(cudaMemsetAsync(chg, 0, sizeof(unsigned long long), s));
         GD_CK(launch_max_change(w.canon(), sc.tmp.as<float>(), w.dist, chg, s));
@@ -873,16 +889,20 @@ Status fill_splitmix(float* out, long long n, unsigned long long seed, cudaStrea
     return Status::Ok();
 }
 
-Status take_watchdog() {
+Status take_deferred() {
     DeviceCtx& dc = device_ctx();
     std::lock_guard<std::mutex> lk(dc.mu);
     if (!dc.err_h) return Status::Ok();
     volatile unsigned int* w = dc.err_h;
-    if (*w == 0u) return Status::Ok();
+    const unsigned int v = *w;
+    if (v == 0u) return Status::Ok();
     *w = 0u;
-    return {kCudaError,
-            "halo watchdog: a strip of the directional-pass kernel waited past the spin limit "
-            "for its neighbour; the results of the work enqueued since the last check are invalid"};
+    if (v & kStatusWatchdog)
+        return {kCudaError,
+                "halo watchdog: a strip of the directional-pass kernel waited past the spin "
+                "limit for its neighbour; the results of the work enqueued since the last check "
+                "are invalid"};
+    return Status::Invalid("generalized_geodesic: mask values must lie in [0, 1]");
 }
 
 int launch_log(LaunchRec* out, int max, bool reset) {

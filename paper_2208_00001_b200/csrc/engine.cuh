@@ -64,8 +64,11 @@ Status generalized_geodesic(const GridDesc& g, int B, const float* img, const fl
                             float* out, double lambda, double nu, int iterations, cudaStream_t s,
                             ScanStats* st);
 // gsf (transforms.cpp:231-238) = erode(dilate(M, theta), theta).  B must be 1.
+// Asynchronous on the device (the erode's empty-complement skip is a device-side
+// gate); sync_stats: synchronise at the end to report complement_empty and rounds.
 Status gsf(const GridDesc& g, const float* img, const float* mask, float* out, double lambda,
-           double nu, int iterations, double theta, cudaStream_t s, ScanStats* st);
+           double nu, int iterations, double theta, cudaStream_t s, ScanStats* st,
+           bool sync_stats);
 // scan_to_fixpoint, parallel engine (scan_parallel.cpp:357-397).  B must be 1.
 Status scan_to_fixpoint(const GridDesc& g, const float* img, float* dist, double lambda,
                         int max_rounds, double tol, cudaStream_t s, ScanStats* st);
@@ -95,11 +98,12 @@ struct LaunchRec {
     int tb;         // temporally blocked variant (halo every two planes)
 };
 constexpr int kLaunchLogMax = 4096;
-// Reads (and clears) this device's halo watchdog word: kCudaError if a sweep
-// launch enqueued since the last call gave up waiting for a neighbour.  Needs
-// no stream synchronisation (mapped host memory); a launch still running may
-// raise it later.
-Status take_watchdog();
+// Reads (and clears) this device's deferred-error word (mapped host memory, no
+// stream synchronisation): kCudaError if a sweep launch enqueued since the last
+// call gave up waiting for a neighbour (halo watchdog), kInvalidArgument if a
+// transform found its soft mask outside [0, 1] (the asynchronous path decides
+// that on the device).  Work still running may raise it later.
+Status take_deferred();
 // Copies up to `max` records (oldest first); returns the number logged.
 int launch_log(LaunchRec* out, int max, bool reset);
 

@@ -27,7 +27,22 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                  : "memory");
 }
 
+// try_wait suspends the warp until the phase completes or the time hint (ns)
+// expires, instead of returning at once and spinning on issue slots the other
+// warps of the scheduler could use.
+#ifndef GD_MBAR_HINT
+#define GD_MBAR_HINT 1000000
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if GD_MBAR_HINT > 0
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "GD_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra GD_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity), "n"(GD_MBAR_HINT)
+        : "memory");
+#else
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "GD_WAIT_%=:\n\t"
@@ -35,6 +50,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "@!p bra GD_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
+#endif
 }
 
 // ---- thread-block clusters (DSMEM halo links) --------------------------------

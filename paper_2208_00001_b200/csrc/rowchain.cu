@@ -41,6 +41,7 @@ __device__ __forceinline__ void cp_async_wait() {
 
 template <int KIND, bool F64>
 __global__ void __launch_bounds__(512, 1) row_chain_kernel(const __grid_constant__ SweepParams p) {
+    if (gate_closed(p)) return;
     constexpr bool kI = KIND != kSpatial;
     extern __shared__ float4 smem4[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

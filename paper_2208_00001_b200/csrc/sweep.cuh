@@ -78,6 +78,10 @@ struct SweepParams {
     long long* trace;         // optional per-warp cycle counters (null in production)
     float* ghost;             // TB: forward ghost rows, [cta][TOP|BOT][n1/2+1][nwv*128]
     const float* image;       // plane-step fallback: intensities (same layout as dist)
+    // Device-side gate (the asynchronous API decides on the device, no host sync):
+    // the launch runs iff (*gate & gate_mask) == gate_want; gate == null: always.
+    const int* gate;
+    int gate_mask, gate_want;
     unsigned int* err;        // watchdog word (mapped host memory): a halo wait that exceeds
                               // the spin limit sets it and every later wait gives up, so a
                               // protocol failure ends the launch and is reported, never hangs
@@ -89,6 +93,17 @@ struct SweepParams {
     double lambda;
     float lambda_f;
 };
+
+// Gate bits written by decide_kernel (aux_kernels.cu) for one transform.
+enum GateBits : int {
+    kGateMaskBad = 1,   // soft mask outside [0, 1]: nothing runs, error reported (deferred)
+    kGateF64 = 2,       // lambda = 1 image whose differences are not exact in f32: f64 path
+    kGateSkip = 4,      // GSF erode with an empty complement: the transform is skipped
+};
+
+__device__ __forceinline__ bool gate_closed(const SweepParams& p) {
+    return p.gate && ((__ldg(p.gate) & p.gate_mask) != p.gate_want);
+}
 
 // Host-side launch (defined in sweep.cu).  R = rows per strip; tb = the
 // temporally blocked variant (halo every two planes; boxes with ghost rows:

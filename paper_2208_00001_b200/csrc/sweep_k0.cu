@@ -1,0 +1,14 @@
+// Instantiation unit: the persistent sweep kernel for cost kind kSpatial, f64 = false
+// (sweep_impl.cuh).  One unit per (kind, f64) so the instances compile in parallel.
+#include "sweep_impl.cuh"
+
+namespace gdb {
+
+cudaError_t sweep_launch_k0(int R, bool tb, const CUtensorMap& tm_d, const CUtensorMap& tm_i,
+                              const SweepParams& p, cudaStream_t stream) {
+    return dispatch_r<kSpatial, false>(R, tb, tm_d, tm_i, p, stream);
+}
+
+int sweep_cores_k0(int R, bool tb, int nwv, int cs) { return dispatch_cores<kSpatial, false>(R, tb, nwv, cs); }
+
+}  // namespace gdb

@@ -22,7 +22,10 @@ CONFIGS = {
     "3d_512_l0": dict(shape=(512, 512, 512), batch=0, lam=0.0, it=4, sp=(1.0, 1.0, 2.5)),
     "3d_512_l05": dict(shape=(512, 512, 512), batch=0, lam=0.5, it=4, sp=(1.0, 1.0, 2.5)),
     "3d_512_l1": dict(shape=(512, 512, 512), batch=0, lam=1.0, it=4, sp=(1.0, 1.0, 2.5)),
-    "gsf_256": dict(shape=(256, 256, 256), batch=0, lam=1.0, it=4, sp=(1.0, 1.0, 1.0), gsf=True),
+    # theta = 2, ball mask of radius 64; the reference's gsf runs
+    # 2 transforms (dilate, erode) unless the complement is empty
+    "gsf_256": dict(shape=(256, 256, 256), batch=0, lam=1.0, it=4, sp=(1.0, 1.0, 1.0), gsf=True,
+                    theta=2.0),
     "batch64_256x256x160": dict(shape=(256, 256, 160), batch=64, lam=1.0, it=4,
                                 sp=(1.0, 1.0, 1.0)),
     "batch64_160x256x256": dict(shape=(160, 256, 256), batch=64, lam=1.0, it=4,
@@ -46,11 +49,16 @@ def run(name, cfg, reps):
     gd.device.fill_splitmix(img, 0x67656F64697374 ^ (len(shape) << 32) ^ shape[-1])
     mask = torch.ones(full, dtype=torch.float32, device="cuda")
     mask[tuple(s // 2 for s in full)] = 0.0
+    if cfg.get("gsf"):
+        zz, yy, xx = torch.meshgrid(*[torch.arange(n, device="cuda") for n in shape], indexing="ij")
+        c = [n // 2 for n in shape]
+        mask = (((zz - c[0]) ** 2 + (yy - c[1]) ** 2 + (xx - c[2]) ** 2) <= 64 * 64).float()
     out = torch.empty_like(img)
 
     def once():
         if cfg.get("gsf"):
-            gd.device.gsf(img, mask, out, cfg["sp"], cfg["lam"], 1e10, cfg["it"], 0.0)
+            st = gd.device.gsf(img, mask, out, cfg["sp"], cfg["lam"], 1e10, cfg["it"], cfg["theta"])
+            cfg["_transforms"] = st.rounds // cfg["it"]
         else:
             gd.device.generalized_geodesic(img, mask, out, cfg["sp"], cfg["lam"], 1e10, cfg["it"],
                                            batch=B or None)
@@ -70,7 +78,7 @@ def run(name, cfg, reps):
     prof = gd.profile_read(reset=True)
     ms = e0.elapsed_time(e1) / reps
     vox = img.numel()
-    passes = (2 * len(shape)) * cfg["it"] * (4 if cfg.get("gsf") else 1)
+    passes = (2 * len(shape)) * cfg["it"] * cfg.get("_transforms", 1)
     gbs = 12.0 * vox * passes / (ms * 1e-3) / 1e9
     split = "  ".join(f"{k}={v[0] / reps:.3f}ms/{v[1] // reps}" for k, v in prof.items() if v[1])
     if os.environ.get("GEODIST_TIME_LOG"):
@@ -94,5 +102,5 @@ if __name__ == "__main__":
     ap.add_argument("--reps", type=int, default=3)
     a = ap.parse_args()
     for n, c in CONFIGS.items():
-        if not a.only or a.only in n:
+        if not a.only or n in a.only.split(","):
             run(n, c, a.reps)
