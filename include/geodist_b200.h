@@ -102,6 +102,58 @@ int gd_parallel_scan(const gd_grid* grid, const float* image, float* dist, doubl
 int gd_scan_to_fixpoint(const gd_grid* grid, const float* image, float* dist, double lambda,
                         int max_rounds, double tol, int mem, void* stream, gd_stats* stats);
 
+/* ScanPolicy (transforms.hpp:24-30) for the parallel engine: NULL or
+ * to_fixpoint = 0 -> `iterations` rounds of the pass sequence; to_fixpoint != 0
+ * -> rounds until the largest change is <= tol, at most max_rounds
+ * (scan_to_fixpoint semantics; one stream synchronisation per round). */
+typedef struct gd_policy {
+    int to_fixpoint;
+    int max_rounds; /* >= 1 */
+    double tol;     /* >= 0 */
+} gd_policy;
+
+/* generalized_geodesic / batched with a ScanPolicy (fixpoint mode: batch == 1). */
+int gd_generalized_geodesic_ex(const gd_grid* grid, int batch, const float* images,
+                               const float* soft_masks, double lambda, double nu, int iterations,
+                               const gd_policy* policy, float* out, int mem, void* stream,
+                               gd_stats* stats);
+
+/* geodesic_distance — replaces geodist::geodesic_distance (transforms.hpp:41-44,
+ * transforms.cpp:127-132): hard seeds where seed_mask >= 0.5 (init_hard_seeds,
+ * :74-89, on the device), then the scan.  No seed -> GD_EMPTY_SEEDS. */
+int gd_geodesic_distance(const gd_grid* grid, const float* image, const float* seed_mask,
+                         double lambda, int iterations, const gd_policy* policy, float* out,
+                         int mem, void* stream, gd_stats* stats);
+
+/* euclidean_distance — replaces geodist::euclidean_distance (transforms.cpp:134-141):
+ * lambda = 0 over a uniform image (no image argument: it is never read). */
+int gd_euclidean_distance(const gd_grid* grid, const float* seed_mask, int iterations,
+                          const gd_policy* policy, float* out, int mem, void* stream,
+                          gd_stats* stats);
+
+/* signed_geodesic — replaces geodist::signed_geodesic (transforms.cpp:160-183):
+ * d(inside seeds [mask >= 0.5]) - d(outside seeds); either set empty ->
+ * GD_EMPTY_SEEDS. */
+int gd_signed_geodesic(const gd_grid* grid, const float* image, const float* mask, double lambda,
+                       int iterations, const gd_policy* policy, float* out, int mem,
+                       void* stream, gd_stats* stats);
+
+/* geodesic_dilate / geodesic_erode — replace geodist::geodesic_dilate / _erode
+ * (transforms.cpp:185-229): binary {0,1} outputs; erode reports an empty
+ * complement in stats->complement_empty (GD_MEM_DEVICE: only when stats != NULL,
+ * which synchronises). */
+int gd_geodesic_dilate(const gd_grid* grid, const float* image, const float* mask, double theta,
+                       double lambda, double nu, int iterations, const gd_policy* policy,
+                       float* out, int mem, void* stream, gd_stats* stats);
+int gd_geodesic_erode(const gd_grid* grid, const float* image, const float* mask, double theta,
+                      double lambda, double nu, int iterations, const gd_policy* policy,
+                      float* out, int mem, void* stream, gd_stats* stats);
+
+/* gsf with a ScanPolicy. */
+int gd_gsf_ex(const gd_grid* grid, const float* image, const float* soft_mask, double lambda,
+              double nu, int iterations, double theta, const gd_policy* policy, float* out,
+              int mem, void* stream, gd_stats* stats);
+
 /* Blend (0 < lambda < 1) arithmetic: 0 = f32 (default; within 1e-6 abs +
  * 1e-5 rel of the reference), 1 = f64 replica of the reference (bit-exact). */
 int gd_set_exact_blend(int on);

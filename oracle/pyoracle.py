@@ -101,6 +101,8 @@ class RefLib(_Base):
         L.ref_signed_geodesic.argtypes = [_i, _ip, _dp, _f32p, _f32p, _d, _i, _i, _f32p]
         L.ref_dijkstra_exact.argtypes = [_i, _ip, _dp, _f32p, _f32p, _d, _f32p]
         L.ref_pass_offsets.argtypes = [_i, _dp, _i, _i, _ip, _dp, _ip]
+        L.ref_transform_ex.argtypes = [_i, _i, _ip, _dp, _f32p, _f32p, _d, _d, _i, _d, _i, _i, _d,
+                                       _i, _f32p, _ip, _ip, _ip]
 
     def _msg(self):
         return self.lib.ref_last_error().decode()
@@ -153,6 +155,25 @@ class RefLib(_Base):
                                                   max_rounds, tol, workers or self.workers,
                                                   C.byref(ru), C.byref(cv), C.byref(lc)))
         return d, ru.value, bool(cv.value), lc.value
+
+    TRANSFORMS = ("generalized_geodesic", "geodesic_distance", "euclidean_distance",
+                  "signed_geodesic", "geodesic_dilate", "geodesic_erode", "gsf")
+
+    def transform(self, which, image, mask, spacing=None, lam=1.0, nu=1e10, iterations=2,
+                  theta=0.0, to_fixpoint=False, max_rounds=100, tol=1e-6, workers=None):
+        """Any transforms.hpp transform with a full ScanPolicy; returns
+        (out, {rounds, converged, complement_empty})."""
+        image, mask = _f32(image), _f32(mask)
+        ndim, dims, sp = _canon(mask, spacing)
+        out = np.empty_like(mask)
+        ru, cv, ce = C.c_int(0), C.c_int(0), C.c_int(0)
+        self._check(self.lib.ref_transform_ex(self.TRANSFORMS.index(which), ndim, dims, sp, image,
+                                              mask, lam, nu, iterations, theta,
+                                              1 if to_fixpoint else 0, max_rounds, tol,
+                                              workers or self.workers, out, C.byref(ru),
+                                              C.byref(cv), C.byref(ce)))
+        return out, {"rounds": ru.value, "converged": bool(cv.value),
+                     "complement_empty": bool(ce.value)}
 
     def dijkstra_exact(self, image, init, spacing=None, lam=1.0):
         image, init = _f32(image), _f32(init)

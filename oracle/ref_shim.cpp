@@ -194,6 +194,43 @@ int ref_signed_geodesic(int ndim, const int* dims, const double* spacing, const 
     });
 }
 
+// Every transform of transforms.hpp under one entry, with a full ScanPolicy
+// (iterations or fixpoint): which = 0 generalized_geodesic, 1 geodesic_distance,
+// 2 euclidean_distance, 3 signed_geodesic, 4 geodesic_dilate, 5 geodesic_erode,
+// 6 gsf.  Reports TransformStats {rounds, converged, complement_empty}.
+int ref_transform_ex(int which, int ndim, const int* dims, const double* spacing,
+                     const float* image, const float* mask, double lambda, double nu,
+                     int iterations, double theta, int to_fixpoint, int max_rounds, double tol,
+                     int workers, float* out, int* rounds, int* converged, int* complement_empty) {
+    return guard([&] {
+        auto im = make(ndim, dims, spacing, image);
+        auto m = make(ndim, dims, spacing, mask);
+        const auto pr = params(lambda, nu, iterations);
+        const auto pol = policy(1, workers, to_fixpoint, max_rounds, tol);
+        geodist::TransformStats st;
+        geodist::ScalarGrid r = [&] {
+            switch (which) {
+                case 0: return geodist::generalized_geodesic(im, m, pr, pol, &st);
+                case 1: return geodist::geodesic_distance(im, m, pr, pol, &st);
+                case 2: return geodist::euclidean_distance(m, iterations, pol, &st);
+                case 3: return geodist::signed_geodesic(im, m, pr, pol, &st);
+                case 4: return geodist::geodesic_dilate(im, m, theta, pr, pol, &st);
+                case 5: return geodist::geodesic_erode(im, m, theta, pr, pol, &st);
+                default: {
+                    geodist::GsfParams gp;
+                    gp.base = pr;
+                    gp.theta = theta;
+                    return geodist::gsf(im, m, gp, pol, &st);
+                }
+            }
+        }();
+        put(r, out);
+        if (rounds) *rounds = st.rounds;
+        if (converged) *converged = st.converged ? 1 : 0;
+        if (complement_empty) *complement_empty = st.complement_empty ? 1 : 0;
+    });
+}
+
 int ref_dijkstra_exact(int ndim, const int* dims, const double* spacing, const float* image,
                        const float* init, double lambda, float* out) {
     return guard([&] {

@@ -22,7 +22,9 @@ __all__ = [
     "GeodistError", "InvalidArgument", "EmptySeedsError", "UnsupportedShape", "CudaError",
     "generalized_geodesic", "generalized_geodesic_batched", "gsf", "directional_pass",
     "parallel_scan", "scan_to_fixpoint", "generalised_geodesic2d", "generalised_geodesic3d",
-    "GSF2d", "GSF3d", "set_exact_blend", "kernel_launches", "device", "LIB_PATH",
+    "GSF2d", "GSF3d", "set_exact_blend", "kernel_launches", "device", "LIB_PATH", "transform",
+    "geodesic_distance", "euclidean_distance", "signed_geodesic", "geodesic_dilate",
+    "geodesic_erode",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -61,6 +63,10 @@ class gd_launch_rec(C.Structure):
                                        "nwu", "cs", "ntu", "nvol", "grid", "tb")]
 
 
+class gd_policy(C.Structure):
+    _fields_ = [("to_fixpoint", C.c_int), ("max_rounds", C.c_int), ("tol", C.c_double)]
+
+
 class gd_stats(C.Structure):
     _fields_ = [("rounds", C.c_int), ("converged", C.c_int), ("complement_empty", C.c_int),
                 ("last_change", C.c_double), ("kernel_launches", C.c_longlong)]
@@ -91,6 +97,14 @@ def lib():
         L.gd_fill_splitmix.argtypes = [fp, C.c_longlong, C.c_ulonglong, vp]
         L.gd_set_device.argtypes = [i]
         L.gd_synchronize.argtypes = [vp]
+        pp = C.POINTER(gd_policy)
+        L.gd_generalized_geodesic_ex.argtypes = [gp, i, fp, fp, d, d, i, pp, fp, i, vp, sp]
+        L.gd_geodesic_distance.argtypes = [gp, fp, fp, d, i, pp, fp, i, vp, sp]
+        L.gd_euclidean_distance.argtypes = [gp, fp, i, pp, fp, i, vp, sp]
+        L.gd_signed_geodesic.argtypes = [gp, fp, fp, d, i, pp, fp, i, vp, sp]
+        L.gd_geodesic_dilate.argtypes = [gp, fp, fp, d, d, d, i, pp, fp, i, vp, sp]
+        L.gd_geodesic_erode.argtypes = [gp, fp, fp, d, d, d, i, pp, fp, i, vp, sp]
+        L.gd_gsf_ex.argtypes = [gp, fp, fp, d, d, i, d, pp, fp, i, vp, sp]
         L.gd_profile_enable.argtypes = [i]
         L.gd_debug_launch_log.argtypes = [C.POINTER(gd_launch_rec), i, i]
         L.gd_profile_read.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_longlong),
@@ -192,6 +206,95 @@ def generalized_geodesic(image, soft_mask, spacing=None, lam=1.0, nu=1e10, itera
     if stats is not None:
         stats.update(rounds=st.rounds, kernel_launches=st.kernel_launches)
     return out
+
+
+def _policy(to_fixpoint, max_rounds, tol):
+    """ScanPolicy{to_fixpoint, max_rounds, tol} (transforms.hpp:24-30) or None."""
+    if not to_fixpoint:
+        return None
+    p = gd_policy()
+    p.to_fixpoint, p.max_rounds, p.tol = 1, int(max_rounds), float(tol)
+    return C.byref(p)
+
+
+def _stats_dict(st):
+    return {"rounds": st.rounds, "converged": bool(st.converged),
+            "complement_empty": bool(st.complement_empty)}
+
+
+def _pair(image, mask, what):
+    image, mask = _f32(image), _f32(mask)
+    if image.shape != mask.shape:
+        raise InvalidArgument(f"{what}: shape mismatch")
+    return image, mask
+
+
+def transform(which, image, mask, spacing=None, lam=1.0, nu=1e10, iterations=2, theta=0.0,
+              to_fixpoint=False, max_rounds=100, tol=1e-6):
+    """Any transforms.hpp transform on the GPU with a full ScanPolicy, mirroring
+    the reference's geodist::<which>; returns (out, stats dict).  which:
+    generalized_geodesic, geodesic_distance, euclidean_distance (image ignored),
+    signed_geodesic, geodesic_dilate, geodesic_erode, gsf."""
+    image, mask = _pair(image, mask, which)
+    g = _grid(mask.shape, spacing)
+    out = np.empty_like(mask)
+    st = gd_stats()
+    pol = _policy(to_fixpoint, max_rounds, tol)
+    L = lib()
+    a = (C.byref(g),)
+    tail = (_ptr(out), GD_MEM_HOST, None, C.byref(st))
+    if which == "generalized_geodesic":
+        rc = L.gd_generalized_geodesic_ex(*a, 1, _ptr(image), _ptr(mask), lam, nu, iterations,
+                                          pol, *tail)
+    elif which == "geodesic_distance":
+        rc = L.gd_geodesic_distance(*a, _ptr(image), _ptr(mask), lam, iterations, pol, *tail)
+    elif which == "euclidean_distance":
+        rc = L.gd_euclidean_distance(*a, _ptr(mask), iterations, pol, *tail)
+    elif which == "signed_geodesic":
+        rc = L.gd_signed_geodesic(*a, _ptr(image), _ptr(mask), lam, iterations, pol, *tail)
+    elif which == "geodesic_dilate":
+        rc = L.gd_geodesic_dilate(*a, _ptr(image), _ptr(mask), theta, lam, nu, iterations, pol,
+                                  *tail)
+    elif which == "geodesic_erode":
+        rc = L.gd_geodesic_erode(*a, _ptr(image), _ptr(mask), theta, lam, nu, iterations, pol,
+                                 *tail)
+    elif which == "gsf":
+        rc = L.gd_gsf_ex(*a, _ptr(image), _ptr(mask), lam, nu, iterations, theta, pol, *tail)
+    else:
+        raise InvalidArgument(f"unknown transform {which!r}")
+    _check(rc)
+    return out, _stats_dict(st)
+
+
+def geodesic_distance(image, seed_mask, spacing=None, lam=1.0, iterations=2, **policy):
+    """geodist::geodesic_distance (transforms.hpp:41-44): hard seeds where mask >= 0.5."""
+    return transform("geodesic_distance", image, seed_mask, spacing, lam, 1e10, iterations,
+                     **policy)[0]
+
+
+def euclidean_distance(seed_mask, spacing=None, iterations=2, **policy):
+    """geodist::euclidean_distance (transforms.cpp:134-141)."""
+    seed_mask = _f32(seed_mask)
+    return transform("euclidean_distance", seed_mask, seed_mask, spacing, 0.0, 1e10, iterations,
+                     **policy)[0]
+
+
+def signed_geodesic(image, mask, spacing=None, lam=1.0, iterations=2, **policy):
+    """geodist::signed_geodesic (transforms.cpp:160-183): d(inside) - d(outside)."""
+    return transform("signed_geodesic", image, mask, spacing, lam, 1e10, iterations,
+                     **policy)[0]
+
+
+def geodesic_dilate(image, mask, theta, spacing=None, lam=1.0, nu=1e10, iterations=2, **policy):
+    """geodist::geodesic_dilate (transforms.cpp:185-202)."""
+    return transform("geodesic_dilate", image, mask, spacing, lam, nu, iterations, theta,
+                     **policy)[0]
+
+
+def geodesic_erode(image, mask, theta, spacing=None, lam=1.0, nu=1e10, iterations=2, **policy):
+    """geodist::geodesic_erode (transforms.cpp:204-229)."""
+    return transform("geodesic_erode", image, mask, spacing, lam, nu, iterations, theta,
+                     **policy)[0]
 
 
 def generalized_geodesic_batched(images, soft_masks, spacing=None, lam=1.0, nu=1e10,

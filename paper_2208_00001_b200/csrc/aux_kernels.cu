@@ -285,6 +285,45 @@ __global__ void gsf_erode_kernel(VolView v, const float* dist, VolView o, float*
     }
 }
 
+// Hard seeds (init_hard_seeds, transforms.cpp:74-89): dist = 0 where the seed
+// test holds, kInfSentinel elsewhere; counts the seeds.  invert: seeds where
+// NOT (m >= 0.5) -- the complement mask's seeds (signed_geodesic's outside).
+__global__ void hard_seed_kernel(VolView mv, const float* mask, VolView dv, float* dist, int invert,
+                                 unsigned long long* n_seeds, long long n) {
+    unsigned long long cnt = 0;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const bool seed = (mask[vox_offset(mv, i)] >= 0.5f) != (invert != 0);
+        dist[vox_offset(dv, i)] = seed ? 0.0f : 1.0e10f;
+        cnt += seed ? 1 : 0;
+    }
+    for (int s = 16; s > 0; s >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, s);
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(n_seeds, cnt);
+}
+
+// kept = threshold_mask(M) = [M >= 0.5]; counts its complement
+// (geodesic_erode's prologue, transforms.cpp:211-219).
+__global__ void threshold_count_kernel(VolView v, const float* mask, float* out,
+                                       unsigned long long* n_complement, long long n) {
+    unsigned long long cnt = 0;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long o = vox_offset(v, i);
+        const bool k = mask[o] >= 0.5f;
+        out[o] = k ? 1.0f : 0.0f;
+        cnt += k ? 0 : 1;
+    }
+    for (int s = 16; s > 0; s >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, s);
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(n_complement, cnt);
+}
+
+// signed_geodesic epilogue (transforms.cpp:176-182): out = d_in - d_out in f32.
+__global__ void subtract_kernel(const float* a, const float* b, float* out, long long n) {
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        out[i] = a[i] - b[i];
+}
+
 __global__ void reset_check_kernel(ImageCheck* c) {
     *c = ImageCheck{-1000, 1000, 0, 0, 0, 0};
 }
@@ -296,9 +335,9 @@ __global__ void reset_check_kernel(ImageCheck* c) {
 // empty-complement skip.  A bad mask also raises the deferred-error bit of the
 // device's status word (mapped host memory).
 __global__ void decide_kernel(const ImageCheck* chk, int check_exact,
-                              const unsigned long long* skip_if_zero, int* gate,
-                              unsigned int* status) {
-    const ImageCheck h = *chk;
+                              const unsigned long long* skip_if_zero, unsigned int status_if_skip,
+                              int* gate, unsigned int* status) {
+    const ImageCheck h = chk ? *chk : ImageCheck{-1000, 1000, 0, 0, 0, 0};
     int g = 0;
     if (h.bad_mask) g |= kGateMaskBad;
     if (check_exact) {
@@ -311,6 +350,7 @@ __global__ void decide_kernel(const ImageCheck* chk, int check_exact,
     if (skip_if_zero && *skip_if_zero == 0ull) g |= kGateSkip;
     *gate = g;
     if ((g & kGateMaskBad) && status) atomicOr_system(status, kStatusMaskBad);
+    if ((g & kGateSkip) && status && status_if_skip) atomicOr_system(status, status_if_skip);
 }
 
 // Fixpoint change: max over voxels of f64(before) - f64(after) (scan_parallel.cpp:386-392).
@@ -436,9 +476,30 @@ cudaError_t launch_gsf_erode(const VolView& v, const float* dist, const VolView&
 }
 
 cudaError_t launch_decide(const ImageCheck* chk, bool check_exact,
-                          const unsigned long long* skip_if_zero, int* gate, unsigned int* status,
-                          cudaStream_t s) {
-    decide_kernel<<<1, 1, 0, s>>>(chk, check_exact ? 1 : 0, skip_if_zero, gate, status);
+                          const unsigned long long* skip_if_zero, unsigned int status_if_skip,
+                          int* gate, unsigned int* status, cudaStream_t s) {
+    decide_kernel<<<1, 1, 0, s>>>(chk, check_exact ? 1 : 0, skip_if_zero, status_if_skip, gate,
+                                  status);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_hard_seeds(const VolView& mv, const float* mask, const VolView& dv, float* dist,
+                              bool invert, unsigned long long* n_seeds, cudaStream_t s) {
+    const long long n = mv.count();
+    hard_seed_kernel<<<grid_for(n, 256), 256, 0, s>>>(mv, mask, dv, dist, invert ? 1 : 0, n_seeds, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_threshold_count(const VolView& v, const float* mask, float* out,
+                                   unsigned long long* n_complement, cudaStream_t s) {
+    const long long n = v.count();
+    threshold_count_kernel<<<grid_for(n, 256), 256, 0, s>>>(v, mask, out, n_complement, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_subtract(const float* a, const float* b, float* out, long long n,
+                            cudaStream_t s) {
+    subtract_kernel<<<grid_for(n, 256), 256, 0, s>>>(a, b, out, n);
     return cudaGetLastError();
 }
 

@@ -38,10 +38,20 @@ cudaError_t launch_gsf_erode(const VolView& v, const float* dist, const VolView&
 // Deferred-error bits of the per-device status word (mapped host memory).
 constexpr unsigned int kStatusWatchdog = 1u;  // a halo wait hit the spin limit
 constexpr unsigned int kStatusMaskBad = 2u;   // a soft mask outside [0, 1]
-// One thread: ImageCheck (+ optional GSF count) -> gate word (sweep.cuh GateBits).
+constexpr unsigned int kStatusEmptySeeds = 4u;  // a hard-seed transform without seeds
+// One thread: ImageCheck (nullable) + optional count -> gate word (sweep.cuh
+// GateBits); a zero count closes the gate (kGateSkip) and raises status_if_skip.
 cudaError_t launch_decide(const ImageCheck* chk, bool check_exact,
-                          const unsigned long long* skip_if_zero, int* gate, unsigned int* status,
-                          cudaStream_t s);
+                          const unsigned long long* skip_if_zero, unsigned int status_if_skip,
+                          int* gate, unsigned int* status, cudaStream_t s);
+// init_hard_seeds on the device (transforms.cpp:74-89), counting the seeds.
+cudaError_t launch_hard_seeds(const VolView& mv, const float* mask, const VolView& dv, float* dist,
+                              bool invert, unsigned long long* n_seeds, cudaStream_t s);
+// out = [M >= 0.5] and the count of its complement (geodesic_erode prologue).
+cudaError_t launch_threshold_count(const VolView& v, const float* mask, float* out,
+                                   unsigned long long* n_complement, cudaStream_t s);
+cudaError_t launch_subtract(const float* a, const float* b, float* out, long long n,
+                            cudaStream_t s);
 cudaError_t launch_max_change(const VolView& v, const float* before, const float* after,
                               unsigned long long* out, cudaStream_t s);
 cudaError_t launch_splitmix(float* out, long long n, unsigned long long seed, cudaStream_t s);

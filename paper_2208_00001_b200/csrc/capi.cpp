@@ -126,6 +126,18 @@ int run(int mem, void* stream, long long n, const float* img, const float* aux, 
     return GD_OK;
 }
 
+int policy_of(const gd_policy* p, gdb::Policy* out) {
+    *out = gdb::Policy{};
+    if (!p || !p->to_fixpoint) return GD_OK;
+    if (p->max_rounds < 1)
+        return fail(GD_INVALID_ARGUMENT, "max_rounds must be >= 1, got " + std::to_string(p->max_rounds));
+    if (!(p->tol >= 0.0)) return fail(GD_INVALID_ARGUMENT, "tol must be >= 0");
+    out->fixpoint = true;
+    out->max_rounds = p->max_rounds;
+    out->tol = p->tol;
+    return GD_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -152,6 +164,133 @@ int gd_generalized_geodesic_batched(const gd_grid* grid, int batch, const float*
                  [&](const float* i, const float* m, float* o, cudaStream_t s) {
                      return gdb::generalized_geodesic(g, batch, i, m, o, lambda, nu, iterations,
                                                       s, &st);
+                 });
+    fill_stats(stats, st);
+    return rc;
+}
+
+int gd_generalized_geodesic_ex(const gd_grid* grid, int batch, const float* images,
+                               const float* soft_masks, double lambda, double nu, int iterations,
+                               const gd_policy* policy, float* out, int mem, void* stream,
+                               gd_stats* stats) {
+    gdb::GridDesc g;
+    if (int rc = grid_of(grid, &g)) return rc;
+    gdb::Policy pol;
+    if (int rc = policy_of(policy, &pol)) return rc;
+    if (batch < 1) return fail(GD_INVALID_ARGUMENT, "batch must be >= 1");
+    if (!images || !soft_masks || !out) return fail(GD_INVALID_ARGUMENT, "null buffer");
+    gdb::ScanStats st;
+    int rc = run(mem, stream, g.voxels() * batch, images, soft_masks, out, false,
+                 [&](const float* i, const float* m, float* o, cudaStream_t s) {
+                     return gdb::generalized_geodesic(g, batch, i, m, o, lambda, nu, iterations,
+                                                      s, &st, pol);
+                 });
+    fill_stats(stats, st);
+    return rc;
+}
+
+int gd_geodesic_distance(const gd_grid* grid, const float* image, const float* seed_mask,
+                         double lambda, int iterations, const gd_policy* policy, float* out,
+                         int mem, void* stream, gd_stats* stats) {
+    gdb::GridDesc g;
+    if (int rc = grid_of(grid, &g)) return rc;
+    gdb::Policy pol;
+    if (int rc = policy_of(policy, &pol)) return rc;
+    if (!image || !seed_mask || !out) return fail(GD_INVALID_ARGUMENT, "null buffer");
+    gdb::ScanStats st;
+    int rc = run(mem, stream, g.voxels(), image, seed_mask, out, false,
+                 [&](const float* i, const float* m, float* o, cudaStream_t s) {
+                     return gdb::geodesic_distance(g, i, m, o, lambda, iterations, pol, s, &st);
+                 });
+    fill_stats(stats, st);
+    return rc;
+}
+
+int gd_euclidean_distance(const gd_grid* grid, const float* seed_mask, int iterations,
+                          const gd_policy* policy, float* out, int mem, void* stream,
+                          gd_stats* stats) {
+    gdb::GridDesc g;
+    if (int rc = grid_of(grid, &g)) return rc;
+    gdb::Policy pol;
+    if (int rc = policy_of(policy, &pol)) return rc;
+    if (!seed_mask || !out) return fail(GD_INVALID_ARGUMENT, "null buffer");
+    gdb::ScanStats st;
+    int rc = run(mem, stream, g.voxels(), nullptr, seed_mask, out, false,
+                 [&](const float*, const float* m, float* o, cudaStream_t s) {
+                     return gdb::euclidean_distance(g, m, o, iterations, pol, s, &st);
+                 });
+    fill_stats(stats, st);
+    return rc;
+}
+
+int gd_signed_geodesic(const gd_grid* grid, const float* image, const float* mask, double lambda,
+                       int iterations, const gd_policy* policy, float* out, int mem,
+                       void* stream, gd_stats* stats) {
+    gdb::GridDesc g;
+    if (int rc = grid_of(grid, &g)) return rc;
+    gdb::Policy pol;
+    if (int rc = policy_of(policy, &pol)) return rc;
+    if (!image || !mask || !out) return fail(GD_INVALID_ARGUMENT, "null buffer");
+    gdb::ScanStats st;
+    int rc = run(mem, stream, g.voxels(), image, mask, out, false,
+                 [&](const float* i, const float* m, float* o, cudaStream_t s) {
+                     return gdb::signed_geodesic(g, i, m, o, lambda, iterations, pol, s, &st);
+                 });
+    fill_stats(stats, st);
+    return rc;
+}
+
+int gd_geodesic_dilate(const gd_grid* grid, const float* image, const float* mask, double theta,
+                       double lambda, double nu, int iterations, const gd_policy* policy,
+                       float* out, int mem, void* stream, gd_stats* stats) {
+    gdb::GridDesc g;
+    if (int rc = grid_of(grid, &g)) return rc;
+    gdb::Policy pol;
+    if (int rc = policy_of(policy, &pol)) return rc;
+    if (!image || !mask || !out) return fail(GD_INVALID_ARGUMENT, "null buffer");
+    gdb::ScanStats st;
+    int rc = run(mem, stream, g.voxels(), image, mask, out, false,
+                 [&](const float* i, const float* m, float* o, cudaStream_t s) {
+                     return gdb::geodesic_dilate(g, i, m, o, lambda, nu, iterations, theta, pol, s,
+                                                 &st);
+                 });
+    fill_stats(stats, st);
+    return rc;
+}
+
+int gd_geodesic_erode(const gd_grid* grid, const float* image, const float* mask, double theta,
+                      double lambda, double nu, int iterations, const gd_policy* policy,
+                      float* out, int mem, void* stream, gd_stats* stats) {
+    gdb::GridDesc g;
+    if (int rc = grid_of(grid, &g)) return rc;
+    gdb::Policy pol;
+    if (int rc = policy_of(policy, &pol)) return rc;
+    if (!image || !mask || !out) return fail(GD_INVALID_ARGUMENT, "null buffer");
+    gdb::ScanStats st;
+    const bool sync_stats = mem != GD_MEM_DEVICE || stats != nullptr;
+    int rc = run(mem, stream, g.voxels(), image, mask, out, false,
+                 [&](const float* i, const float* m, float* o, cudaStream_t s) {
+                     return gdb::geodesic_erode(g, i, m, o, lambda, nu, iterations, theta, pol, s,
+                                                &st, sync_stats);
+                 });
+    fill_stats(stats, st);
+    return rc;
+}
+
+int gd_gsf_ex(const gd_grid* grid, const float* image, const float* soft_mask, double lambda,
+              double nu, int iterations, double theta, const gd_policy* policy, float* out,
+              int mem, void* stream, gd_stats* stats) {
+    gdb::GridDesc g;
+    if (int rc = grid_of(grid, &g)) return rc;
+    gdb::Policy pol;
+    if (int rc = policy_of(policy, &pol)) return rc;
+    if (!image || !soft_mask || !out) return fail(GD_INVALID_ARGUMENT, "null buffer");
+    gdb::ScanStats st;
+    const bool sync_stats = mem != GD_MEM_DEVICE || stats != nullptr;
+    int rc = run(mem, stream, g.voxels(), image, soft_mask, out, false,
+                 [&](const float* i, const float* m, float* o, cudaStream_t s) {
+                     return gdb::gsf(g, i, m, o, lambda, nu, iterations, theta, s, &st,
+                                     sync_stats, pol);
                  });
     fill_stats(stats, st);
     return rc;

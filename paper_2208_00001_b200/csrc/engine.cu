@@ -27,7 +27,9 @@ namespace gdb {
 namespace {
 
 std::atomic<long long> g_launches{0};
-std::atomic<bool> g_exact_blend{false};
+// Blend arithmetic mode; GEODIST_EXACT_BLEND=1 selects the f64 replica at load.
+std::atomic<bool> g_exact_blend{std::getenv("GEODIST_EXACT_BLEND") != nullptr &&
+                                std::atoi(std::getenv("GEODIST_EXACT_BLEND")) == 1};
 
 std::mutex g_log_mu;
 std::vector<LaunchRec> g_log;
@@ -123,7 +125,7 @@ struct StreamCtx {
     Buf halo;
     size_t halo_bytes_zeroed = 0;
     uint32_t tag = 1;  // 0 never matches: freshly zeroed halo words are stale
-    Buf dT, iT, padI, padD, tmp, small, trace, ghost;
+    Buf dT, iT, padI, padD, tmp, prev, small, trace, ghost;
 };
 
 struct DeviceCtx {
@@ -250,7 +252,7 @@ Status check_inputs(StreamCtx& sc, const Work& w, cudaStream_t s, Gate* gate) {
         ProfScope ps(kProfOther, 4.0 * w.B * w.g.voxels(), s);
         GD_CK(launch_image_check(v, w.img, nullptr, dev, s));
     }
-    GD_CK(launch_decide(dev, true, nullptr, gate_word(sc), watchdog_word(device_ctx()), s));
+    GD_CK(launch_decide(dev, true, nullptr, 0u, gate_word(sc), watchdog_word(device_ctx()), s));
     g_launches += 3;
     gate->word = gate_word(sc);
     gate->dual = true;
@@ -647,15 +649,71 @@ Status validate_params(double lambda, double nu, int iterations) {
     return Status::Ok();
 }
 
-// generalized_geodesic on bound device buffers, fully asynchronous: the fused
-// init/check kernel and decide_kernel set the gate word; a bad mask closes it
-// (nothing runs; the error is reported through the device's status word).
-// skip_if_zero (GSF erode): the whole transform is gated off when *skip_if_zero == 0.
+// scan_to_fixpoint's round loop (scan_parallel.cpp:357-397) on bound work:
+// one iteration of the pass sequence per round, then the device max-change
+// reduction; the convergence test is a host decision, one sync per round.
+Status fixpoint_work(StreamCtx& sc, Work& w, double lambda, const Policy& pol, const Gate& gate,
+                     cudaStream_t s, ScanStats* st) {
+    const size_t bytes = static_cast<size_t>(w.B) * w.vol * sizeof(float);
+    GD_ST(sc.prev.ensure(bytes));
+    GD_ST(sc.small.ensure(256));
+    unsigned long long* chg = reinterpret_cast<unsigned long long*>(sc.small.as<char>() + 192);
+    int rounds = 0;
+    double last = 0.0;
+    bool converged = false;
+    while (rounds < pol.max_rounds) {
+        GD_CK(cudaMemcpyAsync(sc.prev.p, w.dist, bytes, cudaMemcpyDeviceToDevice, s));
+        GD_ST(scan_work(sc, w, lambda, 1, gate, s, nullptr));
+        ++rounds;
+        GD_CK(cudaMemsetAsync(chg, 0, sizeof(unsigned long long), s));
+        GD_CK(launch_max_change(w.canon(), sc.prev.as<float>(), w.dist, chg, s));
+        ++g_launches;
+        unsigned long long bits = 0;
+        GD_CK(cudaMemcpyAsync(&bits, chg, sizeof(bits), cudaMemcpyDeviceToHost, s));
+        GD_CK(cudaStreamSynchronize(s));
+        std::memcpy(&last, &bits, sizeof(last));
+        if (last <= pol.tol) {
+            converged = true;
+            break;
+        }
+    }
+    if (st) {
+        st->rounds += rounds;
+        st->converged = st->converged && converged;
+        st->last_change = last;
+    }
+    return Status::Ok();
+}
+
+// run_scan (transforms.cpp:91-125) for the parallel engine on bound work.
+Status run_scan_w(StreamCtx& sc, Work& w, double lambda, int iterations, const Policy& pol,
+                  const Gate& gate, cudaStream_t s, ScanStats* st) {
+    if (pol.fixpoint) return fixpoint_work(sc, w, lambda, pol, gate, s, st);
+    return scan_work(sc, w, lambda, iterations, gate, s, st);
+}
+
+// A gate closed for the whole transform (kGateSkip, e.g. the GSF erode with an
+// empty complement) is also a host fact in fixpoint mode, which synchronises
+// anyway: read it so a skipped transform adds no rounds (transforms.cpp:213-219).
+bool skipped_on_host(StreamCtx& sc, cudaStream_t s) {
+    int g = 0;
+    if (cudaMemcpyAsync(&g, gate_word(sc), sizeof(g), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+        return false;
+    return (g & (kGateSkip | kGateMaskBad)) != 0;
+}
+
+// generalized_geodesic on bound device buffers, asynchronous in iterations
+// mode: the fused init/check kernel and decide_kernel set the gate word; a bad
+// mask closes it (nothing runs; the error is reported through the device's
+// status word).  skip_if_zero (GSF / geodesic_erode): the whole transform is
+// gated off when *skip_if_zero == 0.
 Status generalized_locked(StreamCtx& sc, const GridDesc& g, int B, const float* img,
                           const float* mask, float* out, double lambda, double nu, int iterations,
-                          cudaStream_t s, ScanStats* st,
+                          const Policy& pol, cudaStream_t s, ScanStats* st,
                           const unsigned long long* skip_if_zero = nullptr) {
     GD_ST(validate_params(lambda, nu, iterations));
+    if (pol.fixpoint && B != 1) return Status::Invalid("fixpoint mode takes one grid at a time");
     Work w;
     bool padded = false;
     GD_ST(bind(sc, w, g, B, img, out, false, s, &padded));
@@ -673,13 +731,111 @@ Status generalized_locked(StreamCtx& sc, const GridDesc& g, int B, const float* 
         GD_CK(launch_init_generalized(mv, w.canon(), mask, w.dist, nu, chk,
                                       want_img ? img : nullptr, s));
     }
-    GD_CK(launch_decide(chk, want_img, skip_if_zero, gate_word(sc), watchdog_word(device_ctx()), s));
+    GD_CK(launch_decide(chk, want_img, skip_if_zero, 0u, gate_word(sc), watchdog_word(device_ctx()),
+                        s));
     g_launches += 3;
     Gate gate;
     gate.word = gate_word(sc);
     gate.dual = want_img;
-    GD_ST(scan_work(sc, w, lambda, iterations, gate, s, st));
+    if (!(pol.fixpoint && skipped_on_host(sc, s)))
+        GD_ST(run_scan_w(sc, w, lambda, iterations, pol, gate, s, st));
     if (padded) GD_ST(unbind(w, out, s));
+    return Status::Ok();
+}
+
+// init_hard_seeds + run_scan on the device (geodesic_distance,
+// euclidean_distance and signed_geodesic's two halves, transforms.cpp:74-89,
+// 127-141, 160-183).  Seeds where M >= 0.5 (invert: where not); no seed ->
+// every kernel of the transform is gated off and EmptySeedsError is deferred.
+// img may be null for lambda = 0 (never read).
+Status hard_seeds_locked(StreamCtx& sc, const GridDesc& g, const float* img, const float* seeds,
+                         bool invert, float* out, double lambda, int iterations,
+                         const Policy& pol, cudaStream_t s, ScanStats* st) {
+    GD_ST(validate_params(lambda, 0.0, iterations));
+    Work w;
+    bool padded = false;
+    GD_ST(bind(sc, w, g, 1, img, out, false, s, &padded));
+    GD_ST(sc.small.ensure(256));
+    unsigned long long* cnt = reinterpret_cast<unsigned long long*>(sc.small.as<char>() + 136);
+    VolView mv;
+    mv.D = g.D; mv.H = g.H; mv.W = g.W;
+    mv.zs = static_cast<long long>(g.H) * g.W; mv.ys = g.W; mv.vol = g.D * mv.zs;
+    GD_CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), s));
+    {
+        ProfScope ps(kProfInit, 8.0 * g.voxels(), s);
+        GD_CK(launch_hard_seeds(mv, seeds, w.canon(), w.dist, invert, cnt, s));
+    }
+    const bool want_img = cost_kind(lambda) == kIntensity;
+    ImageCheck* chk = nullptr;
+    if (want_img) {
+        chk = sc.small.as<ImageCheck>();
+        GD_CK(launch_image_check(w.canon(), w.img, nullptr, chk, s));
+        g_launches += 2;
+    }
+    GD_CK(launch_decide(chk, want_img, cnt, kStatusEmptySeeds, gate_word(sc),
+                        watchdog_word(device_ctx()), s));
+    g_launches += 2;
+    Gate gate;
+    gate.word = gate_word(sc);
+    gate.dual = want_img;
+    if (!(pol.fixpoint && skipped_on_host(sc, s)))
+        GD_ST(run_scan_w(sc, w, lambda, iterations, pol, gate, s, st));
+    if (padded) GD_ST(unbind(w, out, s));
+    return Status::Ok();
+}
+
+VolView dense_view(const GridDesc& g) {
+    VolView v;
+    v.D = g.D; v.H = g.H; v.W = g.W; v.ys = g.W; v.zs = static_cast<long long>(g.H) * g.W;
+    v.vol = g.D * v.zs;
+    return v;
+}
+
+// geodesic_dilate (transforms.cpp:185-202): out = [GG(I, complement([M >= 0.5])) <= theta],
+// fused with the erode prologue: *n_complement = |{out == 0}|.
+Status dilate_locked(StreamCtx& sc, const GridDesc& g, const float* img, const float* mask,
+                     float* out, double lambda, double nu, int iterations, double theta,
+                     const Policy& pol, cudaStream_t s, ScanStats* st,
+                     unsigned long long* n_complement) {
+    const VolView v = dense_view(g);
+    GD_ST(sc.tmp.ensure(static_cast<size_t>(g.voxels()) * sizeof(float)));
+    float* tmp = sc.tmp.as<float>();
+    GD_CK(launch_gsf_sources(v, mask, v, tmp, s));
+    ++g_launches;
+    GD_ST(generalized_locked(sc, g, 1, img, tmp, out, lambda, nu, iterations, pol, s, st));
+    GD_CK(cudaMemsetAsync(n_complement, 0, sizeof(unsigned long long), s));
+    GD_CK(launch_gsf_dilate(v, out, out, theta, n_complement, s));
+    ++g_launches;
+    return Status::Ok();
+}
+
+// geodesic_erode (transforms.cpp:204-229) with `out` already holding
+// kept = [M >= 0.5] and *n_complement its complement count: out = [GG(I, kept) > theta],
+// or kept unchanged when the complement is empty (device-side gate).
+Status erode_from_kept(StreamCtx& sc, const GridDesc& g, const float* img, float* out,
+                       double lambda, double nu, int iterations, double theta, const Policy& pol,
+                       cudaStream_t s, ScanStats* st, const unsigned long long* n_complement) {
+    const VolView v = dense_view(g);
+    GD_ST(sc.tmp.ensure(static_cast<size_t>(g.voxels()) * sizeof(float)));
+    float* tmp = sc.tmp.as<float>();
+    GD_ST(generalized_locked(sc, g, 1, img, out, tmp, lambda, nu, iterations, pol, s, st,
+                             n_complement));
+    GD_CK(launch_gsf_erode(v, tmp, v, out, theta, gate_word(sc), s));
+    ++g_launches;
+    return Status::Ok();
+}
+
+// complement_empty / rounds of a possibly skipped erode need the device count.
+Status erode_stats(StreamCtx& sc, const unsigned long long* cnt, int iterations,
+                   const Policy& pol, cudaStream_t s, ScanStats* st) {
+    (void)sc;
+    unsigned long long n_src = 0;
+    GD_CK(cudaMemcpyAsync(&n_src, cnt, sizeof(n_src), cudaMemcpyDeviceToHost, s));
+    GD_CK(cudaStreamSynchronize(s));
+    if (n_src == 0) {
+        st->complement_empty = true;
+        if (!pol.fixpoint) st->rounds -= iterations;  // the gated transform added them
+    }
     return Status::Ok();
 }
 
@@ -786,53 +942,99 @@ Status parallel_scan(const GridDesc& g, int B, const float* img, float* dist, do
 
 Status generalized_geodesic(const GridDesc& g, int B, const float* img, const float* mask,
                             float* out, double lambda, double nu, int iterations, cudaStream_t s,
-                            ScanStats* st) {
+                            ScanStats* st, const Policy& pol) {
     DeviceCtx& dc = device_ctx();
     std::lock_guard<std::mutex> lk(dc.mu);
     StreamCtx& sc = dc.streams[s];
-    return generalized_locked(sc, g, B, img, mask, out, lambda, nu, iterations, s, st);
+    return generalized_locked(sc, g, B, img, mask, out, lambda, nu, iterations, pol, s, st);
+}
+
+Status geodesic_distance(const GridDesc& g, const float* img, const float* seeds, float* out,
+                         double lambda, int iterations, const Policy& pol, cudaStream_t s,
+                         ScanStats* st) {
+    DeviceCtx& dc = device_ctx();
+    std::lock_guard<std::mutex> lk(dc.mu);
+    StreamCtx& sc = dc.streams[s];
+    return hard_seeds_locked(sc, g, img, seeds, false, out, lambda, iterations, pol, s, st);
+}
+
+Status euclidean_distance(const GridDesc& g, const float* seeds, float* out, int iterations,
+                          const Policy& pol, cudaStream_t s, ScanStats* st) {
+    DeviceCtx& dc = device_ctx();
+    std::lock_guard<std::mutex> lk(dc.mu);
+    StreamCtx& sc = dc.streams[s];
+    // lambda = 0 over a uniform image (transforms.cpp:134-141): the spatial
+    // kind never reads intensities, so no image is needed
+    return hard_seeds_locked(sc, g, nullptr, seeds, false, out, 0.0, iterations, pol, s, st);
+}
+
+Status signed_geodesic(const GridDesc& g, const float* img, const float* mask, float* out,
+                       double lambda, int iterations, const Policy& pol, cudaStream_t s,
+                       ScanStats* st) {
+    DeviceCtx& dc = device_ctx();
+    std::lock_guard<std::mutex> lk(dc.mu);
+    StreamCtx& sc = dc.streams[s];
+    const long long n = g.voxels();
+    GD_ST(sc.tmp.ensure(static_cast<size_t>(n) * sizeof(float)));
+    float* d_out = sc.tmp.as<float>();
+    // d_in from the inside seeds [M >= 0.5], d_out from the outside ones
+    GD_ST(hard_seeds_locked(sc, g, img, mask, false, out, lambda, iterations, pol, s, st));
+    GD_ST(hard_seeds_locked(sc, g, img, mask, true, d_out, lambda, iterations, pol, s, st));
+    GD_CK(launch_subtract(out, d_out, out, n, s));
+    ++g_launches;
+    return Status::Ok();
+}
+
+Status geodesic_dilate(const GridDesc& g, const float* img, const float* mask, float* out,
+                       double lambda, double nu, int iterations, double theta, const Policy& pol,
+                       cudaStream_t s, ScanStats* st) {
+    if (!(theta >= 0.0)) return Status::Invalid("theta must be >= 0");
+    GD_ST(validate_params(lambda, nu, iterations));
+    DeviceCtx& dc = device_ctx();
+    std::lock_guard<std::mutex> lk(dc.mu);
+    StreamCtx& sc = dc.streams[s];
+    GD_ST(sc.small.ensure(256));
+    unsigned long long* cnt = reinterpret_cast<unsigned long long*>(sc.small.as<char>() + 128);
+    return dilate_locked(sc, g, img, mask, out, lambda, nu, iterations, theta, pol, s, st, cnt);
+}
+
+Status geodesic_erode(const GridDesc& g, const float* img, const float* mask, float* out,
+                      double lambda, double nu, int iterations, double theta, const Policy& pol,
+                      cudaStream_t s, ScanStats* st, bool sync_stats) {
+    if (!(theta >= 0.0)) return Status::Invalid("theta must be >= 0");
+    GD_ST(validate_params(lambda, nu, iterations));
+    DeviceCtx& dc = device_ctx();
+    std::lock_guard<std::mutex> lk(dc.mu);
+    StreamCtx& sc = dc.streams[s];
+    GD_ST(sc.small.ensure(256));
+    unsigned long long* cnt = reinterpret_cast<unsigned long long*>(sc.small.as<char>() + 128);
+    const VolView v = dense_view(g);
+    GD_CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), s));
+    GD_CK(launch_threshold_count(v, mask, out, cnt, s));
+    ++g_launches;
+    GD_ST(erode_from_kept(sc, g, img, out, lambda, nu, iterations, theta, pol, s, st, cnt));
+    if ((sync_stats || pol.fixpoint) && st) GD_ST(erode_stats(sc, cnt, iterations, pol, s, st));
+    return Status::Ok();
 }
 
 Status gsf(const GridDesc& g, const float* img, const float* mask, float* out, double lambda,
            double nu, int iterations, double theta, cudaStream_t s, ScanStats* st,
-           bool sync_stats) {
+           bool sync_stats, const Policy& pol) {
     GD_ST(validate_params(lambda, nu, iterations));
     if (!(theta >= 0.0)) return Status::Invalid("theta must be >= 0, got " + std::to_string(theta));
     DeviceCtx& dc = device_ctx();
     std::lock_guard<std::mutex> lk(dc.mu);
     StreamCtx& sc = dc.streams[s];
-    const long long n = g.voxels();
-    const size_t bytes = static_cast<size_t>(n) * sizeof(float);
-    GD_ST(sc.tmp.ensure(bytes));
     GD_ST(sc.small.ensure(256));
-    float* tmp = sc.tmp.as<float>();
-    VolView v;
-    v.D = g.D; v.H = g.H; v.W = g.W; v.ys = g.W; v.zs = static_cast<long long>(g.H) * g.W;
-    v.vol = g.D * v.zs;
-    // geodesic_dilate (transforms.cpp:185-202)
-    GD_CK(launch_gsf_sources(v, mask, v, tmp, s));
-    ++g_launches;
-    GD_ST(generalized_locked(sc, g, 1, img, tmp, out, lambda, nu, iterations, s, st));
     unsigned long long* cnt = reinterpret_cast<unsigned long long*>(sc.small.as<char>() + 128);
-    GD_CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), s));
-    GD_CK(launch_gsf_dilate(v, out, out, theta, cnt, s));
-    ++g_launches;
-    // geodesic_erode (transforms.cpp:204-229): gated on the device by the
-    // complement count -- when it is 0 every erode kernel leaves at once and out
-    // keeps K = threshold(dilated), as the reference returns `kept`.
-    GD_ST(generalized_locked(sc, g, 1, img, out, tmp, lambda, nu, iterations, s, st, cnt));
-    GD_CK(launch_gsf_erode(v, tmp, v, out, theta, gate_word(sc), s));
-    ++g_launches;
-    if (sync_stats && st) {
-        // TransformStats::complement_empty (and the erode's rounds) need the count
-        unsigned long long n_src = 0;
-        GD_CK(cudaMemcpyAsync(&n_src, cnt, sizeof(n_src), cudaMemcpyDeviceToHost, s));
-        GD_CK(cudaStreamSynchronize(s));
-        if (n_src == 0) {
-            st->complement_empty = true;
-            st->rounds -= iterations;
-        }
-    }
+    // gsf = geodesic_erode(geodesic_dilate(M, theta), theta) (transforms.cpp:231-238):
+    // the dilate epilogue writes K = [dilated >= 0.5] = dilated and counts its
+    // complement; the erode is gated on the device by that count -- when it is 0
+    // every erode kernel leaves at once and out keeps K, as the reference
+    // returns `kept`.
+    GD_ST(dilate_locked(sc, g, img, mask, out, lambda, nu, iterations, theta, pol, s, st, cnt));
+    GD_ST(erode_from_kept(sc, g, img, out, lambda, nu, iterations, theta, pol, s, st, cnt));
+    if ((sync_stats || pol.fixpoint) && st) GD_ST(erode_stats(sc, cnt, iterations, pol, s, st));
     return Status::Ok();
 }
 
@@ -850,35 +1052,14 @@ Status scan_to_fixpoint(const GridDesc& g, const float* img, float* dist, double
     GD_ST(bind(sc, w, g, 1, img, dist, true, s, &padded));
     Gate gate;
     if (cost_kind(lambda) == kIntensity) GD_ST(check_inputs(sc, w, s, &gate));
-    const size_t bytes = static_cast<size_t>(w.vol) * sizeof(float);
-    GD_ST(sc.tmp.ensure(bytes));
-    GD_ST(sc.small.ensure(256));
-    unsigned long long* chg = reinterpret_cast<unsigned long long*>(sc.small.as<char>() + 192);
     ScanStats local;
     ScanStats* stp = st ? st : &local;
-    stp->converged = false;
-    int rounds = 0;
-    double last = 0.0;
-    // The convergence test is a host decision per round (scan_parallel.cpp:376-395):
-    // this entry synchronises once per round.
-    while (rounds < max_rounds) {
-        GD_CK(cudaMemcpyAsync(sc.tmp.p, w.dist, bytes, cudaMemcpyDeviceToDevice, s));
-        GD_ST(scan_work(sc, w, lambda, 1, gate, s, nullptr));
-        ++rounds;
-        GD_CK(cudaMemsetAsync(chg, 0, sizeof(unsigned long long), s));
-        GD_CK(launch_max_change(w.canon(), sc.tmp.as<float>(), w.dist, chg, s));
-        ++g_launches;
-        unsigned long long bits = 0;
-        GD_CK(cudaMemcpyAsync(&bits, chg, sizeof(bits), cudaMemcpyDeviceToHost, s));
-        GD_CK(cudaStreamSynchronize(s));
-        std::memcpy(&last, &bits, sizeof(last));
-        if (last <= tol) {
-            stp->converged = true;
-            break;
-        }
-    }
-    stp->rounds += rounds;
-    stp->last_change = last;
+    stp->converged = true;
+    Policy pol;
+    pol.fixpoint = true;
+    pol.max_rounds = max_rounds;
+    pol.tol = tol;
+    GD_ST(fixpoint_work(sc, w, lambda, pol, gate, s, stp));
     if (padded) GD_ST(unbind(w, dist, s));
     return Status::Ok();
 }
@@ -902,7 +1083,10 @@ Status take_deferred() {
                 "halo watchdog: a strip of the directional-pass kernel waited past the spin "
                 "limit for its neighbour; the results of the work enqueued since the last check "
                 "are invalid"};
-    return Status::Invalid("generalized_geodesic: mask values must lie in [0, 1]");
+    if (v & kStatusMaskBad)
+        return Status::Invalid("generalized_geodesic: mask values must lie in [0, 1]");
+    return {kEmptySeeds, "no seed cell at or above the 0.5 mask threshold (or, for "
+                         "signed_geodesic, the mask or its complement is empty)"};
 }
 
 int launch_log(LaunchRec* out, int max, bool reset) {

@@ -52,6 +52,15 @@ struct ScanStats {
 void set_exact_blend(bool on);
 bool exact_blend();
 
+// ScanPolicy (transforms.hpp:24-30) for the parallel engine: a fixed number of
+// iterations (default) or rounds to a fixpoint (scan_to_fixpoint semantics:
+// one host synchronisation per round).
+struct Policy {
+    bool fixpoint = false;
+    int max_rounds = 100;
+    double tol = 1e-6;
+};
+
 // --- the hot path -----------------------------------------------------------
 // One directional pass (scan_parallel.cpp:298-318).
 Status directional_pass(const GridDesc& g, int B, const float* img, float* dist, int axis,
@@ -62,13 +71,31 @@ Status parallel_scan(const GridDesc& g, int B, const float* img, float* dist, do
 // generalized_geodesic (transforms.cpp:143-158).
 Status generalized_geodesic(const GridDesc& g, int B, const float* img, const float* mask,
                             float* out, double lambda, double nu, int iterations, cudaStream_t s,
-                            ScanStats* st);
+                            ScanStats* st, const Policy& pol = Policy{});
+// geodesic_distance / euclidean_distance / signed_geodesic (transforms.cpp:127-141,
+// 160-183), hard seeds initialised on the device; no seed -> EmptySeedsError
+// (deferred like every device-side finding).
+Status geodesic_distance(const GridDesc& g, const float* img, const float* seeds, float* out,
+                         double lambda, int iterations, const Policy& pol, cudaStream_t s,
+                         ScanStats* st);
+Status euclidean_distance(const GridDesc& g, const float* seeds, float* out, int iterations,
+                          const Policy& pol, cudaStream_t s, ScanStats* st);
+Status signed_geodesic(const GridDesc& g, const float* img, const float* mask, float* out,
+                       double lambda, int iterations, const Policy& pol, cudaStream_t s,
+                       ScanStats* st);
+// geodesic_dilate / geodesic_erode (transforms.cpp:185-229).
+Status geodesic_dilate(const GridDesc& g, const float* img, const float* mask, float* out,
+                       double lambda, double nu, int iterations, double theta, const Policy& pol,
+                       cudaStream_t s, ScanStats* st);
+Status geodesic_erode(const GridDesc& g, const float* img, const float* mask, float* out,
+                      double lambda, double nu, int iterations, double theta, const Policy& pol,
+                      cudaStream_t s, ScanStats* st, bool sync_stats);
 // gsf (transforms.cpp:231-238) = erode(dilate(M, theta), theta).  B must be 1.
 // Asynchronous on the device (the erode's empty-complement skip is a device-side
 // gate); sync_stats: synchronise at the end to report complement_empty and rounds.
 Status gsf(const GridDesc& g, const float* img, const float* mask, float* out, double lambda,
            double nu, int iterations, double theta, cudaStream_t s, ScanStats* st,
-           bool sync_stats);
+           bool sync_stats, const Policy& pol = Policy{});
 // scan_to_fixpoint, parallel engine (scan_parallel.cpp:357-397).  B must be 1.
 Status scan_to_fixpoint(const GridDesc& g, const float* img, float* dist, double lambda,
                         int max_rounds, double tol, cudaStream_t s, ScanStats* st);

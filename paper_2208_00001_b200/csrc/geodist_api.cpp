@@ -55,25 +55,6 @@ void require_workers(int workers) {
         throw std::invalid_argument("workers must be >= 1, got " + std::to_string(workers));
 }
 
-ScalarGrid threshold_mask(const ScalarGrid& mask) {
-    ScalarGrid out = grid_like(mask, 0.0f);
-    for (std::size_t i = 0; i < mask.size(); ++i) out.data()[i] = mask.data()[i] >= 0.5f ? 1.0f : 0.0f;
-    return out;
-}
-
-ScalarGrid complement_mask(const ScalarGrid& binary) {
-    ScalarGrid out = grid_like(binary, 0.0f);
-    for (std::size_t i = 0; i < binary.size(); ++i)
-        out.data()[i] = binary.data()[i] >= 0.5f ? 0.0f : 1.0f;
-    return out;
-}
-
-std::size_t count_set(const ScalarGrid& binary) {
-    std::size_t n = 0;
-    for (float v : binary.values()) n += v >= 0.5f ? 1 : 0;
-    return n;
-}
-
 ScalarGrid with_spacing(const ScalarGrid& g, std::span<const double> spacing) {
     ScalarGrid out(g.ndim(), g.dims(), spacing, 0.0f);
     std::memcpy(out.data(), g.data(), g.size() * sizeof(float));
@@ -333,11 +314,62 @@ ScalarGrid run_scan(const ScalarGrid& image, ScalarGrid dist, const TransformPar
     return dist;
 }
 
+namespace {
+
+// ScanPolicy -> gd_policy (null for the default iterations mode)
+struct PolicyArg {
+    gd_policy p{};
+    const gd_policy* ptr = nullptr;
+    explicit PolicyArg(const ScanPolicy& pol) {
+        if (pol.to_fixpoint) {
+            p.to_fixpoint = 1;
+            p.max_rounds = pol.max_rounds;
+            p.tol = pol.tol;
+            ptr = &p;
+        }
+    }
+};
+
+void add_stats(TransformStats* stats, const gd_stats& st, bool fixpoint) {
+    if (!stats) return;
+    stats->rounds += st.rounds;
+    if (fixpoint) stats->converged = stats->converged && st.converged != 0;
+    stats->complement_empty = stats->complement_empty || st.complement_empty != 0;
+}
+
+// Host-side checks the reference makes before any compute, shared by the
+// transforms below (engine, workers; the data checks run on the device).
+void require_policy(const ScanPolicy& policy, const char* what) {
+    require_device_engine(policy.engine, what);
+    require_workers(policy.workers);
+    if (policy.to_fixpoint) {
+        if (policy.max_rounds < 1)
+            throw std::invalid_argument("max_rounds must be >= 1, got " +
+                                        std::to_string(policy.max_rounds));
+        if (policy.tol < 0.0) throw std::invalid_argument("tol must be >= 0");
+    }
+}
+
+}  // namespace
+
+// Every transform below runs on the B200 through the C-ABI: hard seeds, soft-mask
+// init, thresholds, counts and the signed subtraction are device kernels; the
+// only host work is the reference's argument validation.
 ScalarGrid geodesic_distance(const ScalarGrid& image, const ScalarGrid& seed_mask,
                              const TransformParams& params, const ScanPolicy& policy,
                              TransformStats* stats) {
     require_match(image, seed_mask, "geodesic_distance");
-    return run_scan(image, init_hard_seeds(seed_mask), params, policy, stats);
+    params.validate();
+    require_policy(policy, "geodesic_distance");
+    ScalarGrid out = grid_like(seed_mask, 0.0f);
+    const gd_grid g = to_gd(image);
+    const PolicyArg pa(policy);
+    gd_stats st{};
+    throw_status(gd_geodesic_distance(&g, image.data(), seed_mask.data(), params.lambda,
+                                      params.iterations, pa.ptr, out.data(), GD_MEM_HOST, nullptr,
+                                      &st));
+    add_stats(stats, st, policy.to_fixpoint);
+    return out;
 }
 
 ScalarGrid euclidean_distance(const ScalarGrid& seed_mask, int iterations,
@@ -345,35 +377,34 @@ ScalarGrid euclidean_distance(const ScalarGrid& seed_mask, int iterations,
     TransformParams params;
     params.lambda = 0.0;
     params.iterations = iterations;
-    const ScalarGrid uniform = grid_like(seed_mask, 0.0f);
-    return run_scan(uniform, init_hard_seeds(seed_mask), params, policy, stats);
+    params.validate();
+    require_policy(policy, "euclidean_distance");
+    ScalarGrid out = grid_like(seed_mask, 0.0f);
+    const gd_grid g = to_gd(seed_mask);
+    const PolicyArg pa(policy);
+    gd_stats st{};
+    throw_status(gd_euclidean_distance(&g, seed_mask.data(), iterations, pa.ptr, out.data(),
+                                       GD_MEM_HOST, nullptr, &st));
+    add_stats(stats, st, policy.to_fixpoint);
+    return out;
 }
 
 ScalarGrid generalized_geodesic(const ScalarGrid& image, const ScalarGrid& soft_mask,
                                 const TransformParams& params, const ScanPolicy& policy,
                                 TransformStats* stats) {
     require_match(image, soft_mask, "generalized_geodesic");
-    for (float v : soft_mask.values())
-        if (!(v >= 0.0f && v <= 1.0f))
-            throw std::invalid_argument("generalized_geodesic: mask values must lie in [0, 1]");
     params.validate();
-    require_device_engine(policy.engine, "generalized_geodesic");
-    require_workers(policy.workers);
-    if (policy.to_fixpoint) {
-        ScalarGrid dist = grid_like(soft_mask, 0.0f);
-        for (std::size_t i = 0; i < soft_mask.size(); ++i) {
-            const double v = params.nu * static_cast<double>(soft_mask.data()[i]);
-            dist.data()[i] = static_cast<float>(std::min(v, static_cast<double>(kInfSentinel)));
-        }
-        return run_scan(image, std::move(dist), params, policy, stats);
-    }
+    require_policy(policy, "generalized_geodesic");
+    // the mask-range check (transforms.cpp:22-28) runs fused with the soft-mask
+    // init on the device and is reported before any result is copied back
     ScalarGrid out = grid_like(soft_mask, 0.0f);
     const gd_grid g = to_gd(image);
+    const PolicyArg pa(policy);
     gd_stats st{};
-    throw_status(gd_generalized_geodesic(&g, image.data(), soft_mask.data(), params.lambda,
-                                         params.nu, params.iterations, out.data(), GD_MEM_HOST,
-                                         nullptr, &st));
-    if (stats) stats->rounds += params.iterations;
+    throw_status(gd_generalized_geodesic_ex(&g, 1, image.data(), soft_mask.data(), params.lambda,
+                                            params.nu, params.iterations, pa.ptr, out.data(),
+                                            GD_MEM_HOST, nullptr, &st));
+    add_stats(stats, st, policy.to_fixpoint);
     return out;
 }
 
@@ -381,14 +412,16 @@ ScalarGrid signed_geodesic(const ScalarGrid& image, const ScalarGrid& mask,
                            const TransformParams& params, const ScanPolicy& policy,
                            TransformStats* stats) {
     require_match(image, mask, "signed_geodesic");
-    const ScalarGrid inside = threshold_mask(mask);
-    const ScalarGrid outside = complement_mask(inside);
-    if (count_set(inside) == 0) throw EmptySeedsError("signed_geodesic: mask is empty");
-    if (count_set(outside) == 0) throw EmptySeedsError("signed_geodesic: mask complement is empty");
-    const ScalarGrid d_in = run_scan(image, init_hard_seeds(inside), params, policy, stats);
-    const ScalarGrid d_out = run_scan(image, init_hard_seeds(outside), params, policy, stats);
+    params.validate();
+    require_policy(policy, "signed_geodesic");
     ScalarGrid out = grid_like(mask, 0.0f);
-    for (std::size_t i = 0; i < out.size(); ++i) out.data()[i] = d_in.data()[i] - d_out.data()[i];
+    const gd_grid g = to_gd(image);
+    const PolicyArg pa(policy);
+    gd_stats st{};
+    throw_status(gd_signed_geodesic(&g, image.data(), mask.data(), params.lambda,
+                                    params.iterations, pa.ptr, out.data(), GD_MEM_HOST, nullptr,
+                                    &st));
+    add_stats(stats, st, policy.to_fixpoint);
     return out;
 }
 
@@ -397,11 +430,16 @@ ScalarGrid geodesic_dilate(const ScalarGrid& image, const ScalarGrid& mask, doub
                            TransformStats* stats) {
     if (!(theta >= 0.0)) throw std::invalid_argument("theta must be >= 0");
     require_match(image, mask, "geodesic_dilate");
-    const ScalarGrid d =
-        generalized_geodesic(image, complement_mask(threshold_mask(mask)), params, policy, stats);
+    params.validate();
+    require_policy(policy, "geodesic_dilate");
     ScalarGrid out = grid_like(mask, 0.0f);
-    for (std::size_t i = 0; i < out.size(); ++i)
-        out.data()[i] = static_cast<double>(d.data()[i]) <= theta ? 1.0f : 0.0f;
+    const gd_grid g = to_gd(image);
+    const PolicyArg pa(policy);
+    gd_stats st{};
+    throw_status(gd_geodesic_dilate(&g, image.data(), mask.data(), theta, params.lambda, params.nu,
+                                    params.iterations, pa.ptr, out.data(), GD_MEM_HOST, nullptr,
+                                    &st));
+    add_stats(stats, st, policy.to_fixpoint);
     return out;
 }
 
@@ -410,15 +448,16 @@ ScalarGrid geodesic_erode(const ScalarGrid& image, const ScalarGrid& mask, doubl
                           TransformStats* stats) {
     if (!(theta >= 0.0)) throw std::invalid_argument("theta must be >= 0");
     require_match(image, mask, "geodesic_erode");
-    const ScalarGrid kept = threshold_mask(mask);
-    if (count_set(complement_mask(kept)) == 0) {
-        if (stats) stats->complement_empty = true;
-        return kept;
-    }
-    const ScalarGrid d = generalized_geodesic(image, kept, params, policy, stats);
+    params.validate();
+    require_policy(policy, "geodesic_erode");
     ScalarGrid out = grid_like(mask, 0.0f);
-    for (std::size_t i = 0; i < out.size(); ++i)
-        out.data()[i] = static_cast<double>(d.data()[i]) > theta ? 1.0f : 0.0f;
+    const gd_grid g = to_gd(image);
+    const PolicyArg pa(policy);
+    gd_stats st{};
+    throw_status(gd_geodesic_erode(&g, image.data(), mask.data(), theta, params.lambda, params.nu,
+                                   params.iterations, pa.ptr, out.data(), GD_MEM_HOST, nullptr,
+                                   &st));
+    add_stats(stats, st, policy.to_fixpoint);
     return out;
 }
 
@@ -426,23 +465,16 @@ ScalarGrid gsf(const ScalarGrid& image, const ScalarGrid& soft_mask, const GsfPa
                const ScanPolicy& policy, TransformStats* stats) {
     params.validate();
     require_match(image, soft_mask, "gsf");
-    if (policy.engine == Engine::Parallel && !policy.to_fixpoint) {
-        require_workers(policy.workers);
-        ScalarGrid out = grid_like(soft_mask, 0.0f);
-        const gd_grid g = to_gd(image);
-        gd_stats st{};
-        throw_status(gd_gsf(&g, image.data(), soft_mask.data(), params.base.lambda, params.base.nu,
-                            params.base.iterations, params.theta, out.data(), GD_MEM_HOST,
-                            nullptr, &st));
-        if (stats) {
-            stats->rounds += st.rounds;
-            stats->complement_empty = stats->complement_empty || st.complement_empty;
-        }
-        return out;
-    }
-    const ScalarGrid dilated =
-        geodesic_dilate(image, soft_mask, params.theta, params.base, policy, stats);
-    return geodesic_erode(image, dilated, params.theta, params.base, policy, stats);
+    require_policy(policy, "gsf");
+    ScalarGrid out = grid_like(soft_mask, 0.0f);
+    const gd_grid g = to_gd(image);
+    const PolicyArg pa(policy);
+    gd_stats st{};
+    throw_status(gd_gsf_ex(&g, image.data(), soft_mask.data(), params.base.lambda, params.base.nu,
+                           params.base.iterations, params.theta, pa.ptr, out.data(), GD_MEM_HOST,
+                           nullptr, &st));
+    add_stats(stats, st, policy.to_fixpoint);
+    return out;
 }
 
 ScalarGrid generalised_geodesic2d(const ScalarGrid& image, const ScalarGrid& softmask, double v,

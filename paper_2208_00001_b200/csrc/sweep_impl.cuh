@@ -40,7 +40,7 @@ __device__ __forceinline__ bool watchdog_raised(const unsigned int* err) {
 #define GD_WATCHDOG 1
 #endif
 #ifndef GD_WARP_INTERLEAVE
-#define GD_WARP_INTERLEAVE 1
+#define GD_WARP_INTERLEAVE 0  // measured within noise at 512^3 (profiles/r02_variants.txt)
 #endif
 #ifndef GD_MINB2
 #define GD_MINB2 3  // R = 4 strips of <= 256 columns: 3 CTAs per SM (batches; measured 97 -> 81 ms)
@@ -538,12 +538,15 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p,
                 // checked every 1024 polls) give up on this neighbour; the host
                 // reports the failure instead of a hang or a sticky trap.
 #if GD_WATCHDOG
-                ++spins;
-                const bool give_up = spins > kSpinLimit ||
-                                     ((spins & 1023) == 0 && watchdog_raised(p.err));
-                if (__any_sync(kFull, give_up)) {
-                    if (lane == 0) watchdog_raise(p.err);
-                    break;
+                // `spins` is warp-uniform (the loop exits on __all_sync), so the
+                // fast path is one increment and compare, as cheap as a trap test;
+                // only a wait far beyond any halo latency (2^14 polls, ~10 ms)
+                // looks at the watchdog word.
+                if (++spins >= (1ll << 14)) {
+                    if (spins > kSpinLimit || ((spins & 1023) == 0 && watchdog_raised(p.err))) {
+                        if (lane == 0) watchdog_raise(p.err);
+                        break;
+                    }
                 }
 #else
                 if (++spins > kSpinLimit) __trap();
