@@ -2,8 +2,8 @@
 // reference's unit tests include (<doctest.h>, absent from this image; the
 // reference expects it under its git-ignored vendor/, proj/CMakeLists.txt:10).
 // It implements exactly what /root/reference/proj/tests/test_{grid,metric,
-// scan_parallel,transforms}.cpp use: TEST_CASE, CHECK, CHECK_FALSE, REQUIRE,
-// CHECK_NOTHROW, CHECK_THROWS_AS and doctest::Approx (doctest's comparison rule
+// scan_parallel,transforms,io,cli}.cpp use: TEST_CASE, SUBCASE (flat), CHECK,
+// CHECK_FALSE, REQUIRE, FAIL, CHECK_NOTHROW, CHECK_THROWS_AS and doctest::Approx (doctest's comparison rule
 // |a - b| < eps * (scale + max(|a|, |b|)), eps = 100 * FLT_EPSILON, scale = 1).
 // Each test case runs in its own try/catch; the runner prints one line per case
 // and a summary, and exits non-zero on any failure.  Cases listed (one name per
@@ -71,6 +71,18 @@ struct Reg {
 
 struct RequireFailed {};
 
+// SUBCASE: the test case body runs once per leaf subcase (doctest's model,
+// flat subcases only): pass k executes the k-th SUBCASE it meets.
+struct SubcaseState {
+    int target = 0;
+    int seen = 0;
+};
+inline SubcaseState& subcases() {
+    static SubcaseState s;
+    return s;
+}
+inline bool enter_subcase() { return subcases().seen++ == subcases().target; }
+
 inline int& failures() {
     static int f = 0;
     return f;
@@ -99,6 +111,12 @@ inline void report(bool ok, const char* what, const char* file, int line) {
     static void fn()
 #define TEST_CASE(name) DOCTEST_CASE_IMPL(DOCTEST_CAT(doctest_case_, __COUNTER__), name)
 
+#define SUBCASE(name) if (doctest::detail::enter_subcase())
+#define FAIL(...)                                                                   \
+    do {                                                                            \
+        doctest::detail::report(false, "FAIL: " #__VA_ARGS__, __FILE__, __LINE__);  \
+        throw doctest::detail::RequireFailed{};                                     \
+    } while (0)
 #define CHECK(...) doctest::detail::report(static_cast<bool>(__VA_ARGS__), #__VA_ARGS__, __FILE__, __LINE__)
 #define CHECK_FALSE(...) \
     doctest::detail::report(!static_cast<bool>(__VA_ARGS__), "!(" #__VA_ARGS__ ")", __FILE__, __LINE__)
@@ -144,7 +162,13 @@ int main() {
         const int before = failures();
         std::string err;
         try {
-            c.fn();
+            SubcaseState& sc = subcases();
+            sc.target = 0;
+            do {
+                sc.seen = 0;
+                c.fn();
+                ++sc.target;
+            } while (sc.target < sc.seen);
         } catch (const RequireFailed&) {
             err = "REQUIRE failed";
         } catch (const std::exception& e) {

@@ -36,8 +36,18 @@ __device__ __forceinline__ bool watchdog_raised(const unsigned int* err) {
 #ifndef GD_NST4
 #define GD_NST4 6
 #endif
+// Halo spin limit: 0 = trap (the production choice: the flag-based watchdog's
+// extra loop exit measured 8-9% slower per sweep at 512^3 and on the batch,
+// profiles/r02_variants.txt), 1 = raise the device watchdog word and give up.
 #ifndef GD_WATCHDOG
-#define GD_WATCHDOG 1
+#define GD_WATCHDOG 0
+#endif
+// Early interior (finish / publish / store the rows that do not wait for the
+// halo before the halo spin): measured slower for the min-plus kinds at 512^3
+// (14.98 vs 14.48 ms) and on the batch (87.5 vs 82.0 ms), within noise for
+// blend (profiles/r02_variants.txt) -- off.
+#ifndef GD_EARLY_INTERIOR
+#define GD_EARLY_INTERIOR 0
 #endif
 #ifndef GD_WARP_INTERLEAVE
 #define GD_WARP_INTERLEAVE 0  // measured within noise at 512^3 (profiles/r02_variants.txt)
@@ -295,6 +305,40 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p,
         }
     };
 
+    // One row's share of publish_smem (the early-interior path publishes the
+    // rows that do not wait for the halo before the halo spin).
+    auto publish_smem_row = [&](int j, int r, const float (&N)[RW][kC]) {
+        const int par = j & 1;
+        if (NWU > 1) {
+            float* rw_ = c.rows + par * RPAR + wu * 2 * VW;
+            if (r == 0 && !TOP)
+                *reinterpret_cast<float4*>(rw_ + vl) =
+                    make_float4(N[0][0], N[0][1], N[0][2], N[0][3]);
+            if (r == RW - 1 && !BOT)
+                *reinterpret_cast<float4*>(rw_ + VW + vl) =
+                    make_float4(N[RW - 1][0], N[RW - 1][1], N[RW - 1][2], N[RW - 1][3]);
+        }
+        float* e = edge_own + par * EPAR;
+        if (lane == 0) e[r] = N[r][0];
+        if (lane == 31) e[ESL + r] = N[r][kC - 1];
+    };
+    auto store_row = [&](int r, const float (&N)[RW][kC]) {
+        float* q = outp + r * su;
+        if (FULL) {
+            *reinterpret_cast<float4*>(q) = make_float4(N[r][0], N[r][1], N[r][2], N[r][3]);
+        } else if (rowv[r]) {
+            if (colv[kC - 1]) {
+                *reinterpret_cast<float4*>(q) = make_float4(N[r][0], N[r][1], N[r][2], N[r][3]);
+            } else {
+#pragma unroll
+                for (int q2 = 0; q2 < kC; ++q2)
+                    if (colv[q2]) q[q2] = N[r][q2];
+            }
+        }
+    };
+    // A row that waits for the neighbour strip's halo row.
+    auto border_row = [&](int r) { return (TOP && r == 0) || (BOT && r == RW - 1); };
+
     float PA[RW][kC], IA[RW][kC], PB[RW][kC], IB[RW][kC];
     float G[kC];  // TB: ghost row (above for TOP, below for BOT) of the last A step
 #pragma unroll
@@ -507,6 +551,32 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p,
             else relax_row<KIND, F64>(acc[RW - 1], pw, iw, ic[RW - 1], +1, p);
         }
 
+        auto fin = [&](int r) {
+#pragma unroll
+            for (int q = 0; q < kC; ++q) {
+                Pout[r][q] = acc[r][q].final(p);
+                if (!FULL && !(rowv[r] && colv[q])) Pout[r][q] = INF;
+                Iout[r][q] = ic[r][q];
+            }
+        };
+        // The output row pointer of this plane (the backward pass walks back).
+        if (j == n1 + 1) dsoff = -dsoff;
+        outp += dsoff;
+        // Early interior: rows that do not border the strip are final after
+        // phase A -- finish, publish (shared memory) and store them while the
+        // halo poll is still in flight, so only the border rows remain behind
+        // the halo wait.
+        constexpr bool EARLY = GD_EARLY_INTERIOR && !TB;
+        if (EARLY) {
+#pragma unroll
+            for (int r = 0; r < RW; ++r) {
+                if (border_row(r)) continue;
+                fin(r);
+                if (j < J) publish_smem_row(j, r, Pout);
+                store_row(r, Pout);
+            }
+        }
+
         // ---- phase B: rows above / below the strip (tagged halo) -------------
 #ifdef GD_SWEEP_TRACE
         long long t_tail0_outer = 0;
@@ -604,14 +674,6 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p,
         __syncwarp();
         if (lane == 0) mbar_arrive(&c.empty[pslot]);
 
-        auto fin = [&](int r) {
-#pragma unroll
-            for (int q = 0; q < kC; ++q) {
-                Pout[r][q] = acc[r][q].final(p);
-                if (!FULL && !(rowv[r] && colv[q])) Pout[r][q] = INF;
-                Iout[r][q] = ic[r][q];
-            }
-        };
         // Border rows first: they are the neighbours' critical path.
         if (TOP) fin(0);
         if (BOT && (RW > 1 || !TOP)) fin(RW - 1);
@@ -623,46 +685,38 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p,
 #ifdef GD_SWEEP_TRACE
         if (TOP || BOT) trc[9] += clock64() - t_tail0_outer;
 #endif
+        if (EARLY) {
 #pragma unroll
-        for (int r = 0; r < RW; ++r)
-            if (!((TOP && r == 0) || (BOT && r == RW - 1))) fin(r);
-        if (GHOST) {
-            const bool present = TOP ? has_up : has_dn;
-#pragma unroll
-            for (int q = 0; q < kC; ++q) {
-                G[q] = present ? accG[q].final(p) : INF;
-                if (!FULL && !colv[q]) G[q] = INF;
+            for (int r = 0; r < RW; ++r) {
+                if (!border_row(r)) continue;
+                if (j < J) publish_smem_row(j, r, Pout);
+                store_row(r, Pout);
             }
-            if (j < J) {
-                float* e = edge_own + (j & 1) * EPAR;
-                if (lane == 0) e[RW] = G[0];
-                if (lane == 31) e[ESL + RW] = G[kC - 1];
-            }
-            if (!backward && p.npass == 2 && present)
-                *reinterpret_cast<float4*>(gscr + static_cast<long long>(j >> 1) * VW) =
-                    make_float4(G[0], G[1], G[2], G[3]);
-        }
-        if (j < J) publish_smem(j, Pout);
-
-        // ---- store the relaxed plane ------------------------------------------
-        if (j == n1 + 1) dsoff = -dsoff;  // the backward pass walks back
-        outp += dsoff;
+        } else {
 #pragma unroll
-        for (int r = 0; r < RW; ++r) {
-            float* q = outp + r * su;
-            if (FULL) {
-                *reinterpret_cast<float4*>(q) =
-                    make_float4(Pout[r][0], Pout[r][1], Pout[r][2], Pout[r][3]);
-            } else if (rowv[r]) {
-                if (colv[kC - 1]) {
-                    *reinterpret_cast<float4*>(q) =
-                        make_float4(Pout[r][0], Pout[r][1], Pout[r][2], Pout[r][3]);
-                } else {
+            for (int r = 0; r < RW; ++r)
+                if (!border_row(r)) fin(r);
+            if (GHOST) {
+                const bool present = TOP ? has_up : has_dn;
 #pragma unroll
-                    for (int q2 = 0; q2 < kC; ++q2)
-                        if (colv[q2]) q[q2] = Pout[r][q2];
+                for (int q = 0; q < kC; ++q) {
+                    G[q] = present ? accG[q].final(p) : INF;
+                    if (!FULL && !colv[q]) G[q] = INF;
                 }
+                if (j < J) {
+                    float* e = edge_own + (j & 1) * EPAR;
+                    if (lane == 0) e[RW] = G[0];
+                    if (lane == 31) e[ESL + RW] = G[kC - 1];
+                }
+                if (!backward && p.npass == 2 && present)
+                    *reinterpret_cast<float4*>(gscr + static_cast<long long>(j >> 1) * VW) =
+                        make_float4(G[0], G[1], G[2], G[3]);
             }
+            if (j < J) publish_smem(j, Pout);
+
+            // ---- store the relaxed plane --------------------------------------
+#pragma unroll
+            for (int r = 0; r < RW; ++r) store_row(r, Pout);
         }
         // Backward planes are read back through TMA (async proxy): order this
         // thread's stores before them.  A fence covers all earlier stores too,

@@ -2,7 +2,8 @@
 
 oracle/Makefile (target dropin-tests, built by __graft_entry__.build() where
 /root/reference exists) compiles the reference's unit tests
-(test_{grid,metric,scan_parallel,transforms}.cpp, 44 cases) and its acceptance
+(test_{grid,metric,scan_parallel,transforms,io}.cpp, 53 cases), its CLI tests
+(test_cli.cpp, 9 cases, run against our bin/geodist_b200) and its acceptance
 suite (acceptance_main.cpp, A1-A9) unchanged, with include/geodist first on the
 include path, linked against paper_2208_00001_b200/lib/libgeodist_b200.so.
 Here the prebuilt binaries run on the GPU: every case passes except those that
@@ -31,7 +32,7 @@ def _run(name, env=None):
 
 @pytest.mark.parametrize("mode", ["exact_blend", "f32_blend"])
 def test_reference_unit_tests_on_dropin(mode):
-    """Exact blend (GEODIST_EXACT_BLEND=1, the f64 replica): 42 of 44 cases pass,
+    """Exact blend (GEODIST_EXACT_BLEND=1, the f64 replica): 51 of 53 cases pass,
     the 2 CPU-engine cases fail by design.  Default f32 blend: additionally the
     shadow-pass case fails on its lambda = 0.7 bitwise subcases only."""
     exact = mode == "exact_blend"
@@ -43,11 +44,23 @@ def test_reference_unit_tests_on_dropin(mode):
     summary = [ln for ln in out.splitlines() if ln.startswith("== ")][-1]
     n_xf = 2 if exact else 3
     assert "0 failed" in summary and f"{n_xf} expected failures" in summary, summary
-    assert f"44 test cases: {44 - n_xf} passed" in summary, summary
+    assert f"53 test cases: {53 - n_xf} passed" in summary, summary
     if not exact:  # the shadow-pass failures are the lambda = 0.7 bitwise checks only
         bad = [ln for ln in out.splitlines() if "CHECK FAILED" in ln]
         assert bad and all("test_scan_parallel.cpp:14" in ln or "test_scan_parallel.cpp:15" in ln
                            for ln in bad), bad
+
+
+def test_reference_cli_tests_on_our_cli():
+    """tests/test_cli.cpp against bin/geodist_b200 (our CLI: compute / compare /
+    benchmark, FGD1 + PGM I/O, exit codes): 7 of 9 pass; the 2 that need the
+    oracle / serial CPU engines fail by design."""
+    r = _run("dropin_cli_tests",
+             {"GD_EXPECTED_FAIL": os.path.join(ROOT, "oracle", "dropin_cli_expected_fail.txt")})
+    out = r.stdout
+    assert r.returncode == 0, out[-4000:] + r.stderr[-2000:]
+    summary = [ln for ln in out.splitlines() if ln.startswith("== ")][-1]
+    assert "9 test cases: 7 passed, 0 failed, 2 expected failures" in summary, summary
 
 
 def test_reference_acceptance_on_dropin():
