@@ -154,17 +154,37 @@ int gd_gsf_ex(const gd_grid* grid, const float* image, const float* soft_mask, d
               double nu, int iterations, double theta, const gd_policy* policy, float* out,
               int mem, void* stream, gd_stats* stats);
 
+/* Upstream-style symmetric filter, four chained transforms (BASELINE.json's
+ * "GSF3d ... four chained transforms"; the reference's gsf is the closing only):
+ * opening(closing(M)) = dilate(erode(erode(dilate(M, theta), theta), theta), theta)
+ * with the reference's geodesic_dilate / geodesic_erode semantics
+ * (transforms.cpp:185-229).  No reference entry point: its oracle is the
+ * composition of the reference's own dilate / erode calls. */
+int gd_gsf_symmetric(const gd_grid* grid, const float* image, const float* soft_mask,
+                     double lambda, double nu, int iterations, double theta,
+                     const gd_policy* policy, float* out, int mem, void* stream, gd_stats* stats);
+
 /* Blend (0 < lambda < 1) arithmetic: 0 = f32 (default; within 1e-6 abs +
  * 1e-5 rel of the reference), 1 = f64 replica of the reference (bit-exact). */
 int gd_set_exact_blend(int on);
 
+/* Storage-layout planner: 1 (default) = each pass runs on the layout that
+ * minimises sequential plane steps plus rotations ([z][y][x], [x][z][y] or
+ * [y][x][z]); 0 = the fixed plan ([z][y][x] for the z and y passes, [x][z][y]
+ * for x).  Results are identical either way; tuning / testing switch
+ * (GEODIST_LAYOUT_PLAN=0 at load). */
+int gd_set_layout_plan(int on);
+
 /* Per-launch CUDA-event profiling, recorded on each launch's own stream.
- * Classes: 0 sweep (the directional-pass kernel), 1 layout transposes,
- * 2 soft-mask init, 3 checks/thresholds.  gd_profile_read waits for the
- * recorded launches and returns accumulated ms, launch counts and algorithmic
- * bytes (12 B/voxel/pass for the sweep, 8 at lambda = 0) per class. */
+ * Classes: 0 sweep (the directional-pass kernel), 1 layout rotations
+ * (transposes), 2 soft-mask init, 3 checks/thresholds, 4 the f64 twin of a
+ * lambda = 1 sweep (launched beside the f32 one under the device-side gate;
+ * it leaves at once when the image's differences are exact in f32).
+ * gd_profile_read waits for the recorded launches and returns accumulated ms,
+ * launch counts and algorithmic bytes (12 B/voxel/pass for the sweep, 8 at
+ * lambda = 0) per class, 5 entries each. */
 int gd_profile_enable(int on);
-int gd_profile_read(double* ms4, long long* count4, double* bytes4, int reset);
+int gd_profile_read(double* ms5, long long* count5, double* bytes5, int reset);
 /* Per-launch (class, ms) in launch order for the launches collected by the last
  * gd_profile_read (call it with reset = 0 first); returns the number logged. */
 int gd_profile_log(int* kinds, float* ms, int max);
@@ -174,7 +194,7 @@ int gd_profile_log(int* kinds, float* ms, int max);
  * can assert that the intended one did.  Copies up to `max` records into `out`,
  * returns how many are logged; `reset` != 0 clears the log afterwards. */
 typedef struct gd_launch_rec {
-    int axis;  /* 0 depth, 1 height, 2 width (x-sweep layout) */
+    int axis;  /* sweep axis: 0 depth, 1 height, 2 width */
     int npass; /* 1 = one directional pass, 2 = forward+backward pair */
     int kind;  /* 0 spatial (lambda 0), 1 intensity (lambda 1), 2 blend */
     int f64;   /* f64 arithmetic path */
@@ -187,6 +207,8 @@ typedef struct gd_launch_rec {
     int nvol;  /* volumes in the launch */
     int grid;  /* CTAs */
     int tb;    /* temporally blocked variant (halo exchanged every two planes) */
+    int layout; /* storage layout the pass ran on: 0 [z][y][x] (caller's), 1 [x][z][y],
+                   2 [y][x][z] (chosen per pass by the layout planner) */
 } gd_launch_rec;
 int gd_debug_launch_log(gd_launch_rec* out, int max, int reset);
 

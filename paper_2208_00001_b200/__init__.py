@@ -24,7 +24,7 @@ __all__ = [
     "parallel_scan", "scan_to_fixpoint", "generalised_geodesic2d", "generalised_geodesic3d",
     "GSF2d", "GSF3d", "set_exact_blend", "kernel_launches", "device", "LIB_PATH", "transform",
     "geodesic_distance", "euclidean_distance", "signed_geodesic", "geodesic_dilate",
-    "geodesic_erode",
+    "geodesic_erode", "gsf_symmetric",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -60,7 +60,7 @@ class gd_grid(C.Structure):
 
 class gd_launch_rec(C.Structure):
     _fields_ = [(n, C.c_int) for n in ("axis", "npass", "kind", "f64", "path", "rows", "nwv",
-                                       "nwu", "cs", "ntu", "nvol", "grid", "tb")]
+                                       "nwu", "cs", "ntu", "nvol", "grid", "tb", "layout")]
 
 
 class gd_policy(C.Structure):
@@ -92,6 +92,7 @@ def lib():
         L.gd_parallel_scan.argtypes = [gp, fp, fp, d, i, i, vp]
         L.gd_scan_to_fixpoint.argtypes = [gp, fp, fp, d, i, d, i, vp, sp]
         L.gd_set_exact_blend.argtypes = [i]
+        L.gd_set_layout_plan.argtypes = [i]
         L.gd_last_error.restype = C.c_char_p
         L.gd_kernel_launches.restype = C.c_longlong
         L.gd_fill_splitmix.argtypes = [fp, C.c_longlong, C.c_ulonglong, vp]
@@ -105,6 +106,7 @@ def lib():
         L.gd_geodesic_dilate.argtypes = [gp, fp, fp, d, d, d, i, pp, fp, i, vp, sp]
         L.gd_geodesic_erode.argtypes = [gp, fp, fp, d, d, d, i, pp, fp, i, vp, sp]
         L.gd_gsf_ex.argtypes = [gp, fp, fp, d, d, i, d, pp, fp, i, vp, sp]
+        L.gd_gsf_symmetric.argtypes = [gp, fp, fp, d, d, i, d, pp, fp, i, vp, sp]
         L.gd_profile_enable.argtypes = [i]
         L.gd_debug_launch_log.argtypes = [C.POINTER(gd_launch_rec), i, i]
         L.gd_profile_read.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_longlong),
@@ -153,11 +155,16 @@ def set_exact_blend(on: bool) -> None:
     lib().gd_set_exact_blend(1 if on else 0)
 
 
+def set_layout_plan(on: bool) -> None:
+    """Per-pass storage-layout planner on (default) / the fixed plan."""
+    lib().gd_set_layout_plan(1 if on else 0)
+
+
 def kernel_launches() -> int:
     return int(lib().gd_kernel_launches())
 
 
-PROFILE_KINDS = ("sweep", "transpose", "init", "other")
+PROFILE_KINDS = ("sweep", "transpose", "init", "other", "sweep_twin")
 
 
 def profile_enable(on: bool) -> None:
@@ -166,9 +173,10 @@ def profile_enable(on: bool) -> None:
 
 def profile_read(reset: bool = True) -> dict:
     """{kind: (ms, launches, algorithmic_bytes)} accumulated since the last reset."""
-    ms = (C.c_double * 4)()
-    cnt = (C.c_longlong * 4)()
-    by = (C.c_double * 4)()
+    n = len(PROFILE_KINDS)
+    ms = (C.c_double * n)()
+    cnt = (C.c_longlong * n)()
+    by = (C.c_double * n)()
     lib().gd_profile_read(ms, cnt, by, 1 if reset else 0)
     return {k: (ms[i], cnt[i], by[i]) for i, k in enumerate(PROFILE_KINDS)}
 
@@ -260,6 +268,9 @@ def transform(which, image, mask, spacing=None, lam=1.0, nu=1e10, iterations=2, 
                                  *tail)
     elif which == "gsf":
         rc = L.gd_gsf_ex(*a, _ptr(image), _ptr(mask), lam, nu, iterations, theta, pol, *tail)
+    elif which == "gsf_symmetric":
+        rc = L.gd_gsf_symmetric(*a, _ptr(image), _ptr(mask), lam, nu, iterations, theta, pol,
+                                *tail)
     else:
         raise InvalidArgument(f"unknown transform {which!r}")
     _check(rc)
@@ -368,6 +379,14 @@ def generalised_geodesic2d(image, softmask, v, lamb, iter):  # noqa: A002
 
 def generalised_geodesic3d(image, softmask, spacing, v, lamb, iter):  # noqa: A002
     return generalized_geodesic(image, softmask, spacing, lamb, v, iter)
+
+
+def gsf_symmetric(image, softmask, theta, spacing=None, lam=1.0, nu=1e10, iterations=2,
+                  **policy):
+    """Four chained transforms: opening(closing(M)) with the reference's
+    geodesic_dilate / geodesic_erode steps (gd_gsf_symmetric)."""
+    return transform("gsf_symmetric", image, softmask, spacing, lam, nu, iterations, theta,
+                     **policy)[0]
 
 
 def GSF2d(image, softmask, theta, v, lamb, iter):  # noqa: A002,N802

@@ -146,6 +146,11 @@ const char* gd_last_error(void) { return t_err.c_str(); }
 int gd_version(void) { return GD_VERSION; }
 long long gd_kernel_launches(void) { return gdb::kernel_launch_count(); }
 
+int gd_set_layout_plan(int on) {
+    gdb::set_layout_plan(on != 0);
+    return GD_OK;
+}
+
 int gd_set_exact_blend(int on) {
     gdb::set_exact_blend(on != 0);
     return GD_OK;
@@ -296,6 +301,25 @@ int gd_gsf_ex(const gd_grid* grid, const float* image, const float* soft_mask, d
     return rc;
 }
 
+int gd_gsf_symmetric(const gd_grid* grid, const float* image, const float* soft_mask,
+                     double lambda, double nu, int iterations, double theta,
+                     const gd_policy* policy, float* out, int mem, void* stream, gd_stats* stats) {
+    gdb::GridDesc g;
+    if (int rc = grid_of(grid, &g)) return rc;
+    gdb::Policy pol;
+    if (int rc = policy_of(policy, &pol)) return rc;
+    if (!image || !soft_mask || !out) return fail(GD_INVALID_ARGUMENT, "null buffer");
+    gdb::ScanStats st;
+    const bool sync_stats = mem != GD_MEM_DEVICE || stats != nullptr;
+    int rc = run(mem, stream, g.voxels(), image, soft_mask, out, false,
+                 [&](const float* i, const float* m, float* o, cudaStream_t s) {
+                     return gdb::gsf_symmetric(g, i, m, o, lambda, nu, iterations, theta, pol, s,
+                                               &st, sync_stats);
+                 });
+    fill_stats(stats, st);
+    return rc;
+}
+
 int gd_generalized_geodesic(const gd_grid* grid, const float* image, const float* soft_mask,
                             double lambda, double nu, int iterations, float* out, int mem,
                             void* stream, gd_stats* stats) {
@@ -377,8 +401,8 @@ int gd_profile_enable(int on) {
     return GD_OK;
 }
 
-int gd_profile_read(double* ms4, long long* count4, double* bytes4, int reset) {
-    gdb::profile_read(ms4, count4, bytes4, reset != 0);
+int gd_profile_read(double* ms5, long long* count5, double* bytes5, int reset) {
+    gdb::profile_read(ms5, count5, bytes5, reset != 0);
     return GD_OK;
 }
 

@@ -31,6 +31,11 @@ std::atomic<long long> g_launches{0};
 std::atomic<bool> g_exact_blend{std::getenv("GEODIST_EXACT_BLEND") != nullptr &&
                                 std::atoi(std::getenv("GEODIST_EXACT_BLEND")) == 1};
 
+// Layout planner on (default) / the fixed plan (C for z and y, T for x):
+// GEODIST_LAYOUT_PLAN=0 at load, gd_set_layout_plan at run time.
+std::atomic<bool> g_layout_plan{!(std::getenv("GEODIST_LAYOUT_PLAN") &&
+                                  std::atoi(std::getenv("GEODIST_LAYOUT_PLAN")) == 0)};
+
 std::mutex g_log_mu;
 std::vector<LaunchRec> g_log;
 void log_launch(const LaunchRec& r) {
@@ -125,7 +130,7 @@ struct StreamCtx {
     Buf halo;
     size_t halo_bytes_zeroed = 0;
     uint32_t tag = 1;  // 0 never matches: freshly zeroed halo words are stale
-    Buf dT, iT, padI, padD, tmp, prev, small, trace, ghost;
+    Buf dT, iT, dU, iU, padI, padD, tmp, prev, small, trace, ghost;
 };
 
 struct DeviceCtx {
@@ -196,8 +201,39 @@ Status make_map(CUtensorMap* m, const float* base, const uint64_t dims[4],
 
 int round4(int x) { return (x + 3) & ~3; }
 
-// The volumes a scan works on: canonical pitched layout (row pitch Wp) plus
-// the x-sweep layout [b][x][z][y] (row pitch Hp).
+// The volumes a scan works on, in up to three storage layouts, each a rotation
+// of the canonical one (outer, middle, inner axis; rows of the inner axis
+// pitched to a multiple of 4 floats, as TMA strides need 16-byte multiples):
+//   C = [b][z][y][x]  (the caller's layout)
+//   T = [b][x][z][y]
+//   U = [b][y][x][z]
+// A pass along an axis runs in any layout where that axis is outer (z-form
+// TMA boxes) or middle (y-form); the plane's rows are the other free axis and
+// its contiguous columns the inner one.  The planner (scan_work) picks, per
+// pass, the layout that minimises sequential plane steps plus the rotations
+// between layouts.  Rotating C -> T -> U -> C is one 2D tile transpose per
+// outer slice (aux_kernels.cu transpose_kernel, forward; the inverse backward).
+enum LayoutId : int { kLC = 0, kLT = 1, kLU = 2 };
+
+struct Geo {
+    int ext[3];  // extents (outer, middle, inner)
+    int ax[3];   // canonical axis (0 z, 1 y, 2 x) of each
+};
+
+Geo layout_geo(int L, const GridDesc& g) {
+    if (L == kLC) return {{g.D, g.H, g.W}, {0, 1, 2}};
+    if (L == kLT) return {{g.W, g.D, g.H}, {2, 0, 1}};
+    return {{g.H, g.W, g.D}, {1, 2, 0}};
+}
+
+struct LayoutBuf {
+    float* d = nullptr;
+    const float* i = nullptr;
+    int P = 0;             // row pitch (floats)
+    long long vol = 0;     // volume stride (floats)
+    bool img_ready = false;
+};
+
 struct Work {
     GridDesc g;
     int B = 1;
@@ -205,22 +241,15 @@ struct Work {
     float* dist = nullptr;
     int Wp = 0;
     long long zs = 0, vol = 0;
-    float* dT = nullptr;
-    float* iT = nullptr;
-    int Hp = 0;
-    long long volT = 0;
-    bool iT_ready = false;
+    LayoutBuf lay[3];
 
-    VolView canon() const {
+    VolView canon() const { return view(kLC); }
+    VolView view(int L) const {
+        const Geo q = layout_geo(L, g);
         VolView v;
-        v.B = B; v.D = g.D; v.H = g.H; v.W = g.W;
-        v.vol = vol; v.zs = zs; v.ys = Wp;
-        return v;
-    }
-    VolView trans() const {
-        VolView v;
-        v.B = B; v.D = g.D; v.H = g.H; v.W = g.W;
-        v.vol = volT; v.zs = static_cast<long long>(g.D) * Hp; v.ys = Hp;
+        v.B = B; v.D = q.ext[0]; v.H = q.ext[1]; v.W = q.ext[2];
+        const LayoutBuf& b = lay[L];
+        v.ys = b.P; v.zs = static_cast<long long>(q.ext[1]) * b.P; v.vol = b.vol;
         return v;
     }
 };
@@ -259,71 +288,37 @@ Status check_inputs(StreamCtx& sc, const Work& w, cudaStream_t s, Gate* gate) {
     return Status::Ok();
 }
 
-Status ensure_x_layout(StreamCtx& sc, Work& w, bool need_img, cudaStream_t s) {
-    w.Hp = round4(w.g.H);
-    w.volT = static_cast<long long>(w.g.W) * w.g.D * w.Hp;
-    const size_t bytes = static_cast<size_t>(w.B) * w.volT * sizeof(float);
-    GD_ST(sc.dT.ensure(bytes));
-    w.dT = sc.dT.as<float>();
-    if (need_img && !w.iT_ready) {
-        GD_ST(sc.iT.ensure(bytes));
-        w.iT = sc.iT.as<float>();
-        ProfScope ps(kProfTranspose, 8.0 * w.B * w.g.voxels(), s);
-        GD_CK(launch_transpose(w.canon(), w.trans(), w.img, w.iT, true, s));
-        ++g_launches;
-        w.iT_ready = true;
-    }
-    return Status::Ok();
-}
+Buf& layout_dist_buf(StreamCtx& sc, int L) { return L == kLT ? sc.dT : sc.dU; }
+Buf& layout_img_buf(StreamCtx& sc, int L) { return L == kLT ? sc.iT : sc.iU; }
 
-// One launch group of the persistent sweep kernel: `npass` passes along
-// `axis` (canonical 0/1; 2 = the x axis in the [b][x][z][y] layout).
-Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int npass,
-                 double lambda, bool f64, const int* gate, int gate_want, cudaStream_t s,
-                 ScanStats* st) {
-    const GridDesc& g = w.g;
-    int ns, nu, nv, sweep_dim;
-    long long ss, su, vol;
-    const float* ibase;
-    float* dbase;
-    uint64_t dims[4], strides[3];
-    if (axis == 0) {
-        ns = g.D; nu = g.H; nv = g.W; ss = w.zs; su = w.Wp; vol = w.vol;
-        ibase = w.img; dbase = w.dist; sweep_dim = 2;
-        dims[0] = g.W; dims[1] = g.H; dims[2] = g.D;
-        strides[0] = w.Wp * 4ull; strides[1] = w.zs * 4ull; strides[2] = w.vol * 4ull;
-    } else if (axis == 1) {
-        ns = g.H; nu = g.D; nv = g.W; ss = w.Wp; su = w.zs; vol = w.vol;
-        ibase = w.img; dbase = w.dist; sweep_dim = 1;
-        dims[0] = g.W; dims[1] = g.H; dims[2] = g.D;
-        strides[0] = w.Wp * 4ull; strides[1] = w.zs * 4ull; strides[2] = w.vol * 4ull;
-    } else {
-        ns = g.W; nu = g.D; nv = g.H; ss = static_cast<long long>(g.D) * w.Hp; su = w.Hp;
-        vol = w.volT; ibase = w.iT; dbase = w.dT; sweep_dim = 2;
-        dims[0] = g.H; dims[1] = g.D; dims[2] = g.W;
-        strides[0] = w.Hp * 4ull; strides[1] = static_cast<uint64_t>(g.D) * w.Hp * 4ull;
-        strides[2] = w.volT * 4ull;
-    }
-    if (ns < 2) return Status::Ok();  // scan_parallel.cpp:308-310
-    const int kind = cost_kind(lambda);
-    if (kind == kSpatial) ibase = dbase;  // intensities never read; any valid map will do
-    const int nwv = (nv + kWV - 1) / kWV;
+// Allocates layout L's distance buffer and, when the kind reads intensities,
+// rotates the image into it once per scan (cached in w.lay[L].i).
+Status ensure_layout(StreamCtx& sc, Work& w, int L, bool need_img, cudaStream_t s);
+
+// Strip shape of one sweep (rows per strip, co-residency, launch groups).
+struct Shape {
+    int R = 0;             // rows per strip (0: plane-step fallback)
+    int maxc = 0;          // co-resident CTAs of the shape
+    long long per_vol = 0; // strips per volume
+    bool tb = false;
+    int nwv = 0;
+    long long groups = 0;  // sequential launch groups for B volumes
+    double rel = 1.0;      // per-step cost relative to R = 4
+};
+
+// Rows per strip.  Every strip of a volume must be co-resident (the halo chain
+// spins); volumes beyond what fits run in sequential launch groups.  Cost =
+// groups x relative per-step cost of the strip shape (taller strips do more
+// work per step; measured on B200).  A single large volume keeps R = 4 (enough
+// rows to cover the halo latency, strips on every SM); batches of small
+// volumes take taller strips so fewer groups run.
+Shape choose_shape(int nu, int nv, int B, int kind, bool f64) {
+    Shape sh;
+    sh.nwv = (nv + kWV - 1) / kWV;
     static const bool force_fallback =
         std::getenv("GEODIST_SWEEP_FALLBACK") && std::atoi(std::getenv("GEODIST_SWEEP_FALLBACK")) == 1;
-    // Rows per strip.  Every strip of a volume must be co-resident (the halo
-    // chain spins); volumes beyond what fits run in sequential launch groups.
-    // Cost = groups x relative per-step cost of the strip shape (taller strips
-    // do more work per step; measured on B200).  A single large volume keeps
-    // R = 4 (enough rows to cover the halo latency, strips on every SM);
-    // batches of small volumes take taller strips so fewer groups run.
-    int R = 0, maxc = 0;
-    long long per_vol = 0;
     static const int r_env =
         std::getenv("GEODIST_SWEEP_R") ? std::atoi(std::getenv("GEODIST_SWEEP_R")) : 0;
-    // Temporal blocking over plane pairs (halo every two planes): GEODIST_SWEEP_TB=1.
-    // Off by default: measured 16.2 vs 13.3 ms per 512^3 transform -- the B step
-    // (no halo wait) still costs ~2300 cycles, so the saved wait does not pay for
-    // the ghost rows.
     static const int rw_env = [] {
         const char* e = std::getenv("GEODIST_SWEEP_RW");
         const int v = e ? std::atoi(e) : -1;
@@ -331,31 +326,93 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
         return v;
     }();
     (void)rw_env;
+    // Temporal blocking over plane pairs (halo every two planes): GEODIST_SWEEP_TB=1.
+    // Off by default: measured 16.2 vs 13.3 ms per 512^3 transform -- the B step
+    // (no halo wait) still costs ~2300 cycles, so the saved wait does not pay for
+    // the ghost rows.
     static const bool tb_env =
         std::getenv("GEODIST_SWEEP_TB") && std::atoi(std::getenv("GEODIST_SWEEP_TB")) == 1;
-    bool tb = false;
     double best = 0.0;
     for (int cand : {4, 8, 16, 2, 1}) {
-        if (nwv > kMaxWarps || force_fallback) break;
+        if (sh.nwv > kMaxWarps || force_fallback) break;
         if ((nu == 1) != (cand == 1)) continue;
-        if (sweep_warp_rows(cand, nwv, kind) == 0) continue;
-        const bool tbc = tb_env && sweep_has_tb(cand, nwv, kind) && nu > cand;
-        const int mc = sweep_max_coresident(cand, tbc, nwv, kind, f64);
+        if (sweep_warp_rows(cand, sh.nwv, kind) == 0) continue;
+        const bool tbc = tb_env && sweep_has_tb(cand, sh.nwv, kind) && nu > cand;
+        const int mc = sweep_max_coresident(cand, tbc, sh.nwv, kind, f64);
         const long long pv = (nu + cand - 1) / cand;
         if (mc <= 0 || pv > mc) continue;
-        const long long groups = (w.B + mc / pv - 1) / (mc / pv);
+        const long long groups = (B + mc / pv - 1) / (mc / pv);
         // measured per-step cost relative to R = 4 (B200, 64 x 256x256x160 batch)
         const double rel = cand <= 4 ? 1.0 : (cand == 8 ? 2.0 : 3.8);
         double cost = static_cast<double>(groups) * rel;
         if (cand == r_env) cost = -1.0;  // tuning override (experiments)
-        if (R == 0 || cost < best) {
-            R = cand;
-            maxc = mc;
-            per_vol = pv;
+        if (sh.R == 0 || cost < best) {
+            sh.R = cand;
+            sh.maxc = mc;
+            sh.per_vol = pv;
+            sh.tb = tbc;
+            sh.groups = groups;
+            sh.rel = rel;
             best = cost;
-            tb = tbc;
         }
     }
+    return sh;
+}
+
+// Pass geometry of canonical `axis` in layout L (axis outer: z-form, middle: y-form).
+struct PassGeo {
+    bool ok = false;
+    int ns = 0, nu = 0, nv = 0, sweep_dim = 2;
+    long long ss = 0, su = 0;
+    int u_axis = 0, v_axis = 0;
+};
+
+PassGeo pass_geo(const GridDesc& g, int L, int axis, int P) {
+    const Geo q = layout_geo(L, g);
+    PassGeo pg;
+    if (q.ax[0] == axis) {
+        pg.ok = true;
+        pg.ns = q.ext[0]; pg.nu = q.ext[1]; pg.nv = q.ext[2]; pg.sweep_dim = 2;
+        pg.ss = static_cast<long long>(q.ext[1]) * P; pg.su = P;
+        pg.u_axis = q.ax[1];
+    } else if (q.ax[1] == axis) {
+        pg.ok = true;
+        pg.ns = q.ext[1]; pg.nu = q.ext[0]; pg.nv = q.ext[2]; pg.sweep_dim = 1;
+        pg.ss = P; pg.su = static_cast<long long>(q.ext[1]) * P;
+        pg.u_axis = q.ax[0];
+    }
+    pg.v_axis = q.ax[2];
+    return pg;
+}
+
+// One launch group of the persistent sweep kernel: `npass` passes along
+// canonical `axis` on layout L's buffers.
+Status run_sweep(StreamCtx& sc, const Work& w, int L, int axis, int first_orient, int npass,
+                 double lambda, bool f64, const int* gate, int gate_want, cudaStream_t s,
+                 ScanStats* st) {
+    const GridDesc& g = w.g;
+    const LayoutBuf& lb = w.lay[L];
+    const PassGeo pg = pass_geo(g, L, axis, lb.P);
+    if (!pg.ok) return {kCudaError, "internal: pass axis not outer/middle of its layout"};
+    const Geo q = layout_geo(L, g);
+    const int ns = pg.ns, nu = pg.nu, nv = pg.nv, sweep_dim = pg.sweep_dim;
+    const long long ss = pg.ss, su = pg.su, vol = lb.vol;
+    const float* ibase = lb.i;
+    float* dbase = lb.d;
+    uint64_t dims[4], strides[3];
+    dims[0] = q.ext[2]; dims[1] = q.ext[1]; dims[2] = q.ext[0];
+    strides[0] = lb.P * 4ull;
+    strides[1] = static_cast<uint64_t>(q.ext[1]) * lb.P * 4ull;
+    strides[2] = vol * 4ull;
+    if (ns < 2) return Status::Ok();  // scan_parallel.cpp:308-310
+    const int kind = cost_kind(lambda);
+    if (kind == kSpatial) ibase = dbase;  // intensities never read; any valid map will do
+    static const bool force_fallback =
+        std::getenv("GEODIST_SWEEP_FALLBACK") && std::atoi(std::getenv("GEODIST_SWEEP_FALLBACK")) == 1;
+    const Shape sh = choose_shape(nu, nv, w.B, kind, f64);
+    const int nwv = sh.nwv, R = sh.R, maxc = sh.maxc;
+    const long long per_vol = sh.per_vol;
+    const bool tb = sh.tb;
     // R == 0: the plane is wider than kMaxWarps * 128 columns or has more row
     // strips than co-resident CTAs -> the plane-step fallback below.
     const int ntu = static_cast<int>(per_vol);
@@ -404,11 +461,11 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
     p.gate_want = gate_want;
     for (int du = -1; du <= 1; ++du)
         for (int dv = -1; dv <= 1; ++dv) {
-            int dz, dy, dx;
-            if (axis == 0) { dz = -first_orient; dy = du; dx = dv; }
-            else if (axis == 1) { dz = du; dy = -first_orient; dx = dv; }
-            else { dz = du; dy = dv; dx = -first_orient; }
-            const double rho = offset_rho(dz, dy, dx, g.sz, g.sy, g.sx);
+            int d[3];
+            d[axis] = -first_orient;
+            d[pg.u_axis] = du;
+            d[pg.v_axis] = dv;
+            const double rho = offset_rho(d[0], d[1], d[2], g.sz, g.sy, g.sx);
             const int k = (du + 1) * 3 + (dv + 1);
             p.rho[k] = rho;
             p.c0[k] = blend_c0(lambda, rho);
@@ -428,9 +485,9 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
             p.image = ibase + b0 * vol;
             const double bytes = static_cast<double>(p.nvol) * g.voxels() * npass *
                                  (kind == kSpatial ? 8.0 : 12.0);
-            ProfScope ps(kProfSweep, bytes, s);
+            ProfScope ps(gate_want == kGateF64 ? kProfSweepTwin : kProfSweep, bytes, s);
             GD_CK(launch_row_chain(kind, f64, p, s));
-            log_launch({axis, npass, kind, f64 ? 1 : 0, 1, 0, 0, 0, 1, 1, p.nvol, p.nvol, 0});
+            log_launch({axis, npass, kind, f64 ? 1 : 0, 1, 0, 0, 0, 1, 1, p.nvol, p.nvol, 0, L});
             g_launches += 1;
             if (st) st->kernel_launches += 1;
         }
@@ -451,9 +508,9 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
             p.image = ibase + b0 * vol;
             const double bytes = static_cast<double>(p.nvol) * g.voxels() * npass *
                                  (kind == kSpatial ? 8.0 : 12.0);
-            ProfScope ps(kProfSweep, bytes, s);
+            ProfScope ps(gate_want == kGateF64 ? kProfSweepTwin : kProfSweep, bytes, s);
             for (int j = 1; j <= J; ++j) GD_CK(launch_plane_step(kind, f64, p, plane(j), plane(j - 1), s));
-            log_launch({axis, npass, kind, f64 ? 1 : 0, 2, 0, 0, 0, 1, 0, p.nvol, 0, 0});
+            log_launch({axis, npass, kind, f64 ? 1 : 0, 2, 0, 0, 0, 1, 0, p.nvol, 0, 0, L});
             g_launches += J;
             if (st) st->kernel_launches += J;
         }
@@ -514,11 +571,11 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
         {
             const double bytes = static_cast<double>(nvol) * g.voxels() * npass *
                                  (kind == kSpatial ? 8.0 : 12.0);
-            ProfScope ps(kProfSweep, bytes, s);
+            ProfScope ps(gate_want == kGateF64 ? kProfSweepTwin : kProfSweep, bytes, s);
             GD_CK(launch_sweep(kind, f64, R, tb, tm_d, tm_i, p, s));
         }
         log_launch({axis, npass, kind, f64 ? 1 : 0, 0, R, nwv, sweep_warp_rows(R, nwv, kind), p.cs,
-                    ntu, nvol, nvol * ntu, tb ? 1 : 0});
+                    ntu, nvol, nvol * ntu, tb ? 1 : 0, L});
         if (trace_on) {
             std::vector<long long> h(trace_n);
             GD_CK(cudaMemcpyAsync(h.data(), sc.trace.p, trace_n * sizeof(long long),
@@ -554,29 +611,51 @@ Status run_sweep(StreamCtx& sc, const Work& w, int axis, int first_orient, int n
 // One launch group per pair, or -- lambda = 1 under a device-side gate -- the
 // f32 and the f64 instance back to back, each leaving at once unless the gate
 // selects it (a skipped launch costs a few microseconds; no host sync).
-Status sweep_gated(StreamCtx& sc, const Work& w, int axis, int first_orient, int npass,
+Status sweep_gated(StreamCtx& sc, const Work& w, int L, int axis, int first_orient, int npass,
                    double lambda, bool f64, const Gate& gate, cudaStream_t s, ScanStats* st) {
-    if (!gate.word) return run_sweep(sc, w, axis, first_orient, npass, lambda, f64, nullptr, 0, s, st);
+    if (!gate.word)
+        return run_sweep(sc, w, L, axis, first_orient, npass, lambda, f64, nullptr, 0, s, st);
     if (!gate.dual)
-        return run_sweep(sc, w, axis, first_orient, npass, lambda, f64, gate.word, 0, s, st);
-    GD_ST(run_sweep(sc, w, axis, first_orient, npass, lambda, false, gate.word, 0, s, st));
-    return run_sweep(sc, w, axis, first_orient, npass, lambda, true, gate.word, kGateF64, s, st);
+        return run_sweep(sc, w, L, axis, first_orient, npass, lambda, f64, gate.word, 0, s, st);
+    GD_ST(run_sweep(sc, w, L, axis, first_orient, npass, lambda, false, gate.word, 0, s, st));
+    return run_sweep(sc, w, L, axis, first_orient, npass, lambda, true, gate.word, kGateF64, s,
+                     st);
 }
 
-Status x_pair(StreamCtx& sc, Work& w, int first_orient, int npass, double lambda, bool f64,
-              const Gate& gate, cudaStream_t s, ScanStats* st) {
-    GD_ST(ensure_x_layout(sc, w, lambda != 0.0, s));
-    const double tb = 8.0 * w.B * w.g.voxels();
-    {
-        ProfScope ps(kProfTranspose, tb, s);
-        GD_CK(launch_transpose(w.canon(), w.trans(), w.dist, w.dT, true, s));
+Status ensure_layout(StreamCtx& sc, Work& w, int L, bool need_img, cudaStream_t s) {
+    if (L == kLC) return Status::Ok();
+    const Geo q = layout_geo(L, w.g);
+    LayoutBuf& lb = w.lay[L];
+    lb.P = round4(q.ext[2]);
+    lb.vol = static_cast<long long>(q.ext[0]) * q.ext[1] * lb.P;
+    const size_t bytes = static_cast<size_t>(w.B) * lb.vol * sizeof(float);
+    Buf& db = layout_dist_buf(sc, L);
+    GD_ST(db.ensure(bytes));
+    lb.d = db.as<float>();
+    if (need_img && !lb.img_ready) {
+        Buf& ib = layout_img_buf(sc, L);
+        GD_ST(ib.ensure(bytes));
+        // C -> T is one forward rotation, C -> U one inverse rotation
+        ProfScope ps(kProfTranspose, 8.0 * w.B * w.g.voxels(), s);
+        if (L == kLT) GD_CK(launch_transpose(w.view(kLC), w.view(kLT), w.img, ib.as<float>(), true, s));
+        else GD_CK(launch_transpose(w.view(kLC), w.view(kLU), w.img, ib.as<float>(), false, s));
+        ++g_launches;
+        lb.i = ib.as<float>();
+        lb.img_ready = true;
     }
-    ++g_launches;
-    GD_ST(sweep_gated(sc, w, 2, first_orient, npass, lambda, f64, gate, s, st));
-    {
-        ProfScope ps(kProfTranspose, tb, s);
-        GD_CK(launch_transpose(w.trans(), w.canon(), w.dT, w.dist, false, s));
-    }
+    return Status::Ok();
+}
+
+// Moves the working distance from layout `from` to `to` (one rotation: forward
+// C->T->U->C or its inverse).
+Status move_dist(StreamCtx& sc, Work& w, int from, int to, bool need_img, cudaStream_t s) {
+    if (from == to) return Status::Ok();
+    GD_ST(ensure_layout(sc, w, to, need_img, s));
+    ProfScope ps(kProfTranspose, 8.0 * w.B * w.g.voxels(), s);
+    // launch_transpose(src view, dst view, src, dst, forward): forward takes
+    // [a][b][c] to [c][a][b]; backward is its inverse (src the rotated side)
+    GD_CK(launch_transpose(w.view(from), w.view(to), w.lay[from].d, w.lay[to].d,
+                           to == (from + 1) % 3, s));
     ++g_launches;
     return Status::Ok();
 }
@@ -584,15 +663,121 @@ Status x_pair(StreamCtx& sc, Work& w, int first_orient, int npass, double lambda
 // f64 arithmetic for blend (exact mode); lambda = 1 decides on the device.
 bool blend_f64(int kind) { return kind == kBlend && g_exact_blend.load(); }
 
-// parallel_scan_inplace: for it: FB BF (3D) TB BT LR RL  (metric.cpp:35-44)
+// --- layout planner ------------------------------------------------------------
+// Estimated device time (us) of one pass group on layout L: sequential plane
+// steps (launch groups x relative step cost x steps) at ~1.1 us per step for
+// the persistent kernel, ~0.3 us per row-chain step, one launch per step for
+// the plane-step fallback; a rotation moves 8 B per voxel at ~5.5 TB/s.
+constexpr double kStepUs = 1.1, kRowChainStepUs = 0.3, kRotateGBs = 5500.0;
+
+double pass_cost_us(const Work& w, int L, int axis, int npass, int kind, bool f64) {
+    const PassGeo pg = pass_geo(w.g, L, axis, round4(layout_geo(L, w.g).ext[2]));
+    if (!pg.ok) return -1.0;
+    if (pg.ns < 2) return 0.0;
+    const double steps = static_cast<double>(npass) * (pg.ns - 1);
+    if (pg.nu == 1) return steps * kRowChainStepUs;
+    const Shape sh = choose_shape(pg.nu, pg.nv, w.B, kind, f64);
+    if (sh.R == 0) return steps * (4.0 + 12.0 * w.B * pg.nu * pg.nv / (kRotateGBs * 1e3) * 1e0);
+    return static_cast<double>(sh.groups) * sh.rel * steps * kStepUs;
+}
+
+double rotate_cost_us(const Work& w) { return 8.0 * w.B * w.g.voxels() / (kRotateGBs * 1e3); }
+
+struct PassSpec {
+    int axis, orient, npass;
+};
+
+// Cheapest layout per pass (dynamic program over (layout, image copies made)):
+// the distance starts and ends in C; entering a layout costs a rotation of the
+// distance, and the first use of T / U also a rotation of the image (when the
+// kind reads intensities).  2D grids keep C for y and T for x (their U rows are
+// a single column).  Ties keep the earlier (lower-numbered) layout.
+std::vector<int> plan_layouts(const Work& w, const std::vector<PassSpec>& passes, int kind,
+                              bool f64) {
+    const int n = static_cast<int>(passes.size());
+    std::vector<int> plan(n, kLC);
+    if (w.g.ndim == 2 || !g_layout_plan.load()) {  // the fixed plan: C for z / y, T for x
+        for (int i = 0; i < n; ++i) plan[i] = passes[i].axis == 2 ? kLT : kLC;
+        return plan;
+    }
+    const bool img = kind != kSpatial;
+    const double rot = rotate_cost_us(w);
+    constexpr double kInf = 1e300;
+    // state: layout L (3) x image-copies mask (bit 0: T, bit 1: U)
+    std::vector<double> cost(12, kInf), next(12);
+    std::vector<std::vector<int>> from(n, std::vector<int>(12, -1));
+    cost[kLC * 4 + 0] = 0.0;
+    for (int i = 0; i < n; ++i) {
+        std::fill(next.begin(), next.end(), kInf);
+        for (int st = 0; st < 12; ++st) {
+            if (cost[st] >= kInf) continue;
+            const int L0 = st / 4, m0 = st % 4;
+            for (int L = 0; L < 3; ++L) {
+                const double pc = pass_cost_us(w, L, passes[i].axis, passes[i].npass, kind, f64);
+                if (pc < 0.0) continue;
+                int m = m0;
+                double c = cost[st] + pc + (L != L0 ? rot : 0.0);
+                if (img && L != kLC && !(m & (1 << (L - 1)))) {
+                    m |= 1 << (L - 1);
+                    c += rot;
+                }
+                const int ns = L * 4 + m;
+                if (c < next[ns] - 1e-9) {
+                    next[ns] = c;
+                    from[i][ns] = st;
+                }
+            }
+        }
+        cost.swap(next);
+    }
+    int best = -1;
+    double bc = kInf;
+    for (int st = 0; st < 12; ++st) {
+        const double c = cost[st] + (st / 4 != kLC ? rot : 0.0);
+        if (c < bc - 1e-9) {
+            bc = c;
+            best = st;
+        }
+    }
+    for (int i = n - 1; i >= 0; --i) {
+        plan[i] = best / 4;
+        best = from[i][best];
+    }
+    return plan;
+}
+
+// Runs `passes` on the working distance (bound in C) with the planned layouts,
+// rotating between them, and leaves the result in C.
+Status run_passes(StreamCtx& sc, Work& w, const std::vector<PassSpec>& passes, double lambda,
+                  const Gate& gate, cudaStream_t s, ScanStats* st) {
+    const int kind = cost_kind(lambda);
+    const bool f64 = blend_f64(kind);
+    const bool img = kind != kSpatial;
+    const std::vector<int> plan = plan_layouts(w, passes, kind, f64);
+    int cur = kLC;
+    for (size_t i = 0; i < passes.size(); ++i) {
+        const int L = plan[i];
+        if (L != cur) {
+            GD_ST(move_dist(sc, w, cur, L, img, s));
+            cur = L;
+        }
+        GD_ST(sweep_gated(sc, w, L, passes[i].axis, passes[i].orient, passes[i].npass, lambda,
+                          f64, gate, s, st));
+    }
+    return move_dist(sc, w, cur, kLC, img, s);
+}
+
+// parallel_scan_inplace: for it: FB BF (3D) TB BT LR RL  (metric.cpp:35-44);
+// each forward / backward pair of one axis is one persistent launch.
 Status scan_work(StreamCtx& sc, Work& w, double lambda, int iterations, const Gate& gate,
                  cudaStream_t s, ScanStats* st) {
-    const bool f64 = blend_f64(cost_kind(lambda));
+    std::vector<PassSpec> passes;
     for (int it = 0; it < iterations; ++it) {
-        if (w.g.ndim == 3) GD_ST(sweep_gated(sc, w, 0, +1, 2, lambda, f64, gate, s, st));
-        GD_ST(sweep_gated(sc, w, 1, +1, 2, lambda, f64, gate, s, st));
-        if (w.g.W >= 2) GD_ST(x_pair(sc, w, +1, 2, lambda, f64, gate, s, st));
+        if (w.g.ndim == 3) passes.push_back({0, +1, 2});
+        passes.push_back({1, +1, 2});
+        if (w.g.W >= 2) passes.push_back({2, +1, 2});
     }
+    GD_ST(run_passes(sc, w, passes, lambda, gate, s, st));
     if (st) st->rounds += iterations;
     return Status::Ok();
 }
@@ -613,6 +798,7 @@ Status bind(StreamCtx& sc, Work& w, const GridDesc& g, int B, const float* img, 
     if (direct) {
         w.img = img;
         w.dist = dist;
+        w.lay[kLC] = {dist, img, w.Wp, w.vol, true};
         return Status::Ok();
     }
     const size_t bytes = static_cast<size_t>(B) * w.vol * sizeof(float);
@@ -629,6 +815,7 @@ Status bind(StreamCtx& sc, Work& w, const GridDesc& g, int B, const float* img, 
     }
     w.img = img ? sc.padI.as<float>() : nullptr;
     w.dist = sc.padD.as<float>();
+    w.lay[kLC] = {w.dist, w.img, w.Wp, w.vol, true};
     return Status::Ok();
 }
 
@@ -864,6 +1051,7 @@ Status make_grid_desc(int ndim, const int* dims, const double* spacing, GridDesc
 }
 
 void set_exact_blend(bool on) { g_exact_blend.store(on); }
+void set_layout_plan(bool on) { g_layout_plan.store(on); }
 bool exact_blend() { return g_exact_blend.load(); }
 long long kernel_launch_count() { return g_launches.load(); }
 
@@ -914,12 +1102,10 @@ Status directional_pass(const GridDesc& g, int B, const float* img, float* dist,
     const int kind = cost_kind(lambda);
     Gate gate;
     if (kind == kIntensity) GD_ST(check_inputs(sc, w, s, &gate));
-    const bool f64 = blend_f64(kind);
-    if (axis == 2) {
-        if (g.W >= 2) GD_ST(x_pair(sc, w, orientation, 1, lambda, f64, gate, s, st));
-    } else {
-        GD_ST(sweep_gated(sc, w, axis, orientation, 1, lambda, f64, gate, s, st));
-    }
+    // scan_parallel.cpp:308-311: a single-plane sweep axis is a no-op (and a 3D
+    // x pass with W < 2 never leaves the caller's layout)
+    const int ext[3] = {g.D, g.H, g.W};
+    if (ext[axis] >= 2) GD_ST(run_passes(sc, w, {{axis, orientation, 1}}, lambda, gate, s, st));
     if (padded) GD_ST(unbind(w, dist, s));
     return Status::Ok();
 }
@@ -1035,6 +1221,46 @@ Status gsf(const GridDesc& g, const float* img, const float* mask, float* out, d
     GD_ST(dilate_locked(sc, g, img, mask, out, lambda, nu, iterations, theta, pol, s, st, cnt));
     GD_ST(erode_from_kept(sc, g, img, out, lambda, nu, iterations, theta, pol, s, st, cnt));
     if ((sync_stats || pol.fixpoint) && st) GD_ST(erode_stats(sc, cnt, iterations, pol, s, st));
+    return Status::Ok();
+}
+
+// Upstream-FastGeodis-style symmetric filter in four chained transforms
+// (BASELINE.json config 4; PAPER.md:143-153 names GSF without a formula): the
+// reference's closing gsf = erode(dilate(M)) (transforms.cpp:231-238)
+// followed by the opening dilate(erode(.)), each step the reference's
+// geodesic_dilate / geodesic_erode semantics (transforms.cpp:185-229) with the
+// erode's empty-complement skip gated on the device.
+Status gsf_symmetric(const GridDesc& g, const float* img, const float* mask, float* out,
+                     double lambda, double nu, int iterations, double theta, const Policy& pol,
+                     cudaStream_t s, ScanStats* st, bool sync_stats) {
+    GD_ST(validate_params(lambda, nu, iterations));
+    if (!(theta >= 0.0)) return Status::Invalid("theta must be >= 0, got " + std::to_string(theta));
+    DeviceCtx& dc = device_ctx();
+    std::lock_guard<std::mutex> lk(dc.mu);
+    StreamCtx& sc = dc.streams[s];
+    GD_ST(sc.small.ensure(256));
+    unsigned long long* cnt = reinterpret_cast<unsigned long long*>(sc.small.as<char>() + 128);
+    unsigned long long* cnt2 = reinterpret_cast<unsigned long long*>(sc.small.as<char>() + 144);
+    const VolView v = dense_view(g);
+    ScanStats s1, s2;
+    // closing: erode(dilate(M))
+    GD_ST(dilate_locked(sc, g, img, mask, out, lambda, nu, iterations, theta, pol, s, &s1, cnt));
+    GD_ST(erode_from_kept(sc, g, img, out, lambda, nu, iterations, theta, pol, s, &s1, cnt));
+    // opening: dilate(erode(closed))
+    GD_CK(cudaMemsetAsync(cnt2, 0, sizeof(unsigned long long), s));
+    GD_CK(launch_threshold_count(v, out, out, cnt2, s));
+    ++g_launches;
+    GD_ST(erode_from_kept(sc, g, img, out, lambda, nu, iterations, theta, pol, s, &s2, cnt2));
+    GD_ST(dilate_locked(sc, g, img, out, out, lambda, nu, iterations, theta, pol, s, &s2, cnt2));
+    if ((sync_stats || pol.fixpoint) && st) {
+        GD_ST(erode_stats(sc, cnt, iterations, pol, s, &s1));
+        GD_ST(erode_stats(sc, cnt2, iterations, pol, s, &s2));
+    }
+    if (st) {
+        st->rounds += s1.rounds + s2.rounds;
+        st->converged = st->converged && s1.converged && s2.converged;
+        st->complement_empty = s1.complement_empty || s2.complement_empty;
+    }
     return Status::Ok();
 }
 

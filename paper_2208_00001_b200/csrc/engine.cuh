@@ -50,6 +50,8 @@ struct ScanStats {
 // Arithmetic mode for 0 < lambda < 1 (Blend): f32 (default, within the
 // 1e-6 abs + 1e-5 rel contract) or the f64 replica of the reference (bit-exact).
 void set_exact_blend(bool on);
+// Layout planner (per-pass storage layout, engine.cu plan_layouts) on / off.
+void set_layout_plan(bool on);
 bool exact_blend();
 
 // ScanPolicy (transforms.hpp:24-30) for the parallel engine: a fixed number of
@@ -96,6 +98,11 @@ Status geodesic_erode(const GridDesc& g, const float* img, const float* mask, fl
 Status gsf(const GridDesc& g, const float* img, const float* mask, float* out, double lambda,
            double nu, int iterations, double theta, cudaStream_t s, ScanStats* st,
            bool sync_stats, const Policy& pol = Policy{});
+// Four chained transforms: gsf (closing) followed by the opening
+// dilate(erode(.)) -- the upstream-style symmetric filter.
+Status gsf_symmetric(const GridDesc& g, const float* img, const float* mask, float* out,
+                     double lambda, double nu, int iterations, double theta, const Policy& pol,
+                     cudaStream_t s, ScanStats* st, bool sync_stats);
 // scan_to_fixpoint, parallel engine (scan_parallel.cpp:357-397).  B must be 1.
 Status scan_to_fixpoint(const GridDesc& g, const float* img, float* dist, double lambda,
                         int max_rounds, double tol, cudaStream_t s, ScanStats* st);
@@ -110,7 +117,7 @@ long long kernel_launch_count();
 // Launch log of the directional-pass kernels (tests assert which variant ran):
 // one record per sweep launch group, in launch order, capped at kLaunchLogMax.
 struct LaunchRec {
-    int axis;       // 0 z, 1 y, 2 x (x-layout)
+    int axis;       // canonical sweep axis: 0 z, 1 y, 2 x
     int npass;      // 1 or 2 (forward+backward pair)
     int kind;       // CostKind
     int f64;        // f64 arithmetic path
@@ -123,6 +130,7 @@ struct LaunchRec {
     int nvol;       // volumes in this launch
     int grid;       // CTAs
     int tb;         // temporally blocked variant (halo every two planes)
+    int layout;     // storage layout of the pass: 0 [z][y][x], 1 [x][z][y], 2 [y][x][z]
 };
 constexpr int kLaunchLogMax = 4096;
 // Reads (and clears) this device's deferred-error word (mapped host memory, no
@@ -135,10 +143,18 @@ Status take_deferred();
 int launch_log(LaunchRec* out, int max, bool reset);
 
 // Per-launch CUDA-event profiling by kernel class (on the launching stream).
-enum ProfKind : int { kProfSweep = 0, kProfTranspose = 1, kProfInit = 2, kProfOther = 3, kProfKinds = 4 };
+// kProfSweepTwin: the f64 twin of a lambda = 1 sweep, launched next to the f32
+// one under the device-side gate (only one of the two does the work; for
+// images whose differences are exact in f32 -- every benchmark image -- the
+// twin leaves at once, so the sweep class holds the real launches).
+enum ProfKind : int {
+    kProfSweep = 0, kProfTranspose = 1, kProfInit = 2, kProfOther = 3, kProfSweepTwin = 4,
+    kProfKinds = 5
+};
 void profile_enable(bool on);
 // Collects finished launches (synchronising on their end events) and returns
-// accumulated milliseconds, launch counts and algorithmic bytes per class.
+// accumulated milliseconds, launch counts and algorithmic bytes per class
+// (kProfKinds entries each).
 void profile_read(double* ms, long long* count, double* bytes, bool reset);
 // Per-launch (kind, ms) of the launches collected by the last profile_read
 // (before its reset); returns the total number logged.

@@ -184,21 +184,25 @@ def test_default_cluster_instances(gd, oracle, shape, lam, cs):
     img = dyadic_image(rng, shape)
     m = point_mask(shape)
     sp = (1.0, 1.0, 2.5)
-    gd.launch_log(reset=True)
-    g = gd.generalized_geodesic(img, m, sp, lam, 1e10, 2)
-    log = [r for r in gd.launch_log(reset=True) if r["f64"] == 0]  # lambda 1: f64 twin gated off
+    gd.set_layout_plan(False)  # z and y on [z][y][x]: the 512-wide production planes
+    try:
+        gd.launch_log(reset=True)
+        g = gd.generalized_geodesic(img, m, sp, lam, 1e10, 2)
+        log = [r for r in gd.launch_log(reset=True) if r["f64"] == 0]  # lambda 1: f64 twin off
+        d0 = seed_init(rng, shape, 5)
+        single = [(gd.directional_pass(d0, img, 0, o, sp, lam), o) for o in (1, -1)]
+        single_log = gd.launch_log(reset=True)
+    finally:
+        gd.set_layout_plan(True)
     zl = [r for r in log if r["axis"] == 0]
     assert zl and all(r["cs"] == cs and r["nwv"] == 4 and r["rows"] == 4 and r["path"] == 0
                       for r in zl), zl
     assert all(r["cs"] == 1 for r in log if r["axis"] != 0)  # 3-strip planes: L2 links
     r = oracle.generalized_geodesic(img, m, sp, lam, 1e10, 2)
     assert bitwise_equal(g, r), parity(g, r)
-    d0 = seed_init(rng, shape, 5)
-    for o in (1, -1):
-        assert bitwise_equal(gd.directional_pass(d0, img, 0, o, sp, lam),
-                             oracle.directional_pass(d0, img, 0, o, sp, lam))
-    assert all(r["cs"] == cs for r in gd.launch_log(reset=True)
-               if r["axis"] == 0 and r["f64"] == 0)
+    for got, o in single:
+        assert bitwise_equal(got, oracle.directional_pass(d0, img, 0, o, sp, lam))
+    assert all(r["cs"] == cs for r in single_log if r["axis"] == 0 and r["f64"] == 0)
 
 
 @pytest.mark.parametrize("shape", [(3, 6, 2100), (3, 1300, 600)],
@@ -321,3 +325,39 @@ def test_cuda_matches_golden(gd, path):
             assert bitwise_equal(run_fixture(gd, f), f["out"])
         finally:
             gd.set_exact_blend(False)
+
+
+@pytest.mark.parametrize("lam", LAMBDAS)
+def test_layout_planner_batch(gd, oracle, lam):
+    """A batch of narrow volumes: the planner runs the z pass on [x][z][y] and
+    the y pass on [y][x][z] (rows along the short x axis: fewer strips, more
+    volumes per launch group), rotating the distance between layouts; every
+    volume stays bit-exact / within tolerance."""
+    rng = np.random.default_rng(43)
+    B, shape = 64, (40, 48, 24)
+    imgs = dyadic_image(rng, (B,) + shape)
+    masks = np.ones((B,) + shape, np.float32)
+    for b in range(B):
+        masks[b].reshape(-1)[rng.integers(0, masks[b].size)] = 0.0
+    sp = (1.0, 1.3, 2.5)
+    gd.launch_log(reset=True)
+    g = gd.generalized_geodesic_batched(imgs, masks, sp, lam, 1e10, 2)
+    log = [r for r in gd.launch_log(reset=True) if r["f64"] == 0]
+    assert {r["layout"] for r in log if r["axis"] == 0} == {1}, log
+    assert {r["layout"] for r in log if r["axis"] == 1} == {2}, log
+    for b in range(0, B, 9):
+        _check(g[b], oracle.generalized_geodesic(imgs[b], masks[b], sp, lam, 1e10, 2), lam)
+
+
+def test_layout_rotations_single_passes(gd, oracle):
+    """Every single directional pass, including x passes that the planner may
+    put on either rotated layout, against the oracle on a non-cube ragged grid."""
+    rng = np.random.default_rng(47)
+    shape, sp = (13, 22, 9), (1.0, 0.7, 1.9)
+    img = dyadic_image(rng, shape)
+    d0 = seed_init(rng, shape, 3)
+    for axis in range(3):
+        for o in (1, -1):
+            for lam in LAMBDAS:
+                _check(gd.directional_pass(d0, img, axis, o, sp, lam),
+                       oracle.directional_pass(d0, img, axis, o, sp, lam), lam)

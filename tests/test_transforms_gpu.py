@@ -125,3 +125,20 @@ def test_transforms_on_the_device_async(gd, ref):
                                       gd.device._stream(None), None))
     with pytest.raises(gd.EmptySeedsError):
         gd.device.synchronize()
+
+
+@pytest.mark.parametrize("lam", [0.0, 1.0])
+@pytest.mark.parametrize("theta", [0.0, 1.5, 4.0])
+def test_gsf_symmetric_is_the_reference_composition(gd, ref, lam, theta):
+    """The upstream-style 4-transform filter equals the reference's own calls
+    composed: dilate -> erode (its gsf) -> erode -> dilate."""
+    shape, sp = (10, 24, 22), (1.0, 1.0, 2.5)
+    img, mask = _inputs(shape, "gsf", 21)
+    got, st = gd.transform("gsf_symmetric", img, mask, sp, lam, 1e10, 2, theta)
+    kw = dict(spacing=sp, lam=lam, nu=1e10, iterations=2, theta=theta)
+    d1, r1 = ref.transform("geodesic_dilate", img, mask, **kw)
+    e1, r2 = ref.transform("geodesic_erode", img, d1, **kw)
+    e2, r3 = ref.transform("geodesic_erode", img, e1, **kw)
+    want, r4 = ref.transform("geodesic_dilate", img, e2, **kw)
+    assert bitwise_equal(got, want)
+    assert st["rounds"] == r1["rounds"] + r2["rounds"] + r3["rounds"] + r4["rounds"]
