@@ -336,7 +336,7 @@ Shape choose_shape(int nu, int nv, int B, int kind, bool f64) {
     for (int cand : {4, 8, 16, 2, 1}) {
         if (sh.nwv > kMaxWarps || force_fallback) break;
         if ((nu == 1) != (cand == 1)) continue;
-        if (sweep_warp_rows(cand, sh.nwv, kind) == 0) continue;
+        if (sweep_warp_rows(cand, sh.nwv, kind, f64) == 0) continue;
         const bool tbc = tb_env && sweep_has_tb(cand, sh.nwv, kind) && nu > cand;
         const int mc = sweep_max_coresident(cand, tbc, sh.nwv, kind, f64);
         const long long pv = (nu + cand - 1) / cand;
@@ -574,14 +574,14 @@ Status run_sweep(StreamCtx& sc, const Work& w, int L, int axis, int first_orient
             ProfScope ps(gate_want == kGateF64 ? kProfSweepTwin : kProfSweep, bytes, s);
             GD_CK(launch_sweep(kind, f64, R, tb, tm_d, tm_i, p, s));
         }
-        log_launch({axis, npass, kind, f64 ? 1 : 0, 0, R, nwv, sweep_warp_rows(R, nwv, kind), p.cs,
+        log_launch({axis, npass, kind, f64 ? 1 : 0, 0, R, nwv, sweep_warp_rows(R, nwv, kind, f64), p.cs,
                     ntu, nvol, nvol * ntu, tb ? 1 : 0, L});
         if (trace_on) {
             std::vector<long long> h(trace_n);
             GD_CK(cudaMemcpyAsync(h.data(), sc.trace.p, trace_n * sizeof(long long),
                                   cudaMemcpyDeviceToHost, s));
             GD_CK(cudaStreamSynchronize(s));
-            const int nw = nwv * sweep_warp_rows(R, nwv, kind);
+            const int nw = nwv * sweep_warp_rows(R, nwv, kind, f64);
             for (int w = 0; w < nw; ++w) {
                 double acc[12] = {};
                 long long n = 0;
@@ -742,6 +742,19 @@ std::vector<int> plan_layouts(const Work& w, const std::vector<PassSpec>& passes
     for (int i = n - 1; i >= 0; --i) {
         plan[i] = best / 4;
         best = from[i][best];
+    }
+    static const bool dbg = std::getenv("GEODIST_LAYOUT_DEBUG") != nullptr;
+    if (dbg) {
+        std::fprintf(stderr, "layout plan B=%d D=%d H=%d W=%d kind=%d rot=%.1fus total=%.1fus:", w.B,
+                     w.g.D, w.g.H, w.g.W, kind, rot, bc);
+        for (int i = 0; i < n; ++i) {
+            std::fprintf(stderr, " [axis %d -> L%d (", passes[i].axis, plan[i]);
+            for (int L = 0; L < 3; ++L)
+                std::fprintf(stderr, "%s%.0f", L ? "/" : "",
+                             pass_cost_us(w, L, passes[i].axis, passes[i].npass, kind, f64));
+            std::fprintf(stderr, ")]");
+        }
+        std::fprintf(stderr, "\n");
     }
     return plan;
 }

@@ -47,9 +47,9 @@ cudaError_t launch_plane_step(int kind, bool f64, const SweepParams& p, int s, i
 
 void sweep_set_rows_per_warp(int rw) { g_sweep_rw = rw; }
 
-int sweep_warp_rows(int R, int nwv, int kind) {
+int sweep_warp_rows(int R, int nwv, int kind, bool f64) {
     const int mw = width_class(nwv);
-    RwSel sel(R, mw, false, preferred_rw(kind));
+    RwSel sel(R, mw, false, preferred_rw(kind, f64));
 #define GD_CASE(RWW, NW, MM, NS, T, C) \
     if (R == RWW * NW && mw == MM && !T && !C && sel.ok(RWW)) return NW;
     GD_SWEEP_CASES(GD_CASE)

@@ -112,7 +112,7 @@ __device__ __forceinline__ bool gate_closed(const SweepParams& p) {
 cudaError_t launch_sweep(int kind, bool f64, int R, bool tb, const CUtensorMap& tm_d,
                          const CUtensorMap& tm_i, const SweepParams& p, cudaStream_t stream);
 // Warp rows (NWU) of the strip shape serving R rows at this width; 0 = none.
-int sweep_warp_rows(int R, int nwv, int kind);
+int sweep_warp_rows(int R, int nwv, int kind, bool f64 = false);
 // Fallback for planes the persistent kernel cannot hold co-resident (more row
 // strips than CTAs, or wider than kMaxWarps * 128 columns): one launch per
 // plane step, plane s relaxed from plane sp, all `p.nvol` volumes at once.

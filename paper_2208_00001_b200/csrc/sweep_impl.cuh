@@ -46,6 +46,11 @@ __device__ __forceinline__ bool watchdog_raised(const unsigned int* err) {
 // halo before the halo spin): measured slower for the min-plus kinds at 512^3
 // (14.98 vs 14.48 ms) and on the batch (87.5 vs 82.0 ms), within noise for
 // blend (profiles/r02_variants.txt) -- off.
+// Protocol-checking build (make variant V=checks DEFS=-DGD_SWEEP_CHECKS=1):
+// asserts on the halo hand-off invariants; never in production.
+#ifndef GD_SWEEP_CHECKS
+#define GD_SWEEP_CHECKS 0
+#endif
 #ifndef GD_EARLY_INTERIOR
 #define GD_EARLY_INTERIOR 0
 #endif
@@ -586,6 +591,22 @@ __device__ __forceinline__ void consumer_loop(const SweepParams& p,
                 bool ok = (!edge_l || tag_of(h[0]) == want) && (!edge_r || tag_of(h[5]) == want);
 #pragma unroll
                 for (int i = 1; i <= kC; ++i) ok = ok && tag_of(h[i]) == want;
+#if GD_SWEEP_CHECKS
+                // Protocol check (checks build): two parities allow a neighbour at
+                // most one step of skew, so a word tagged beyond `want` means it
+                // overwrote a row this strip had not read yet.
+                bool ahead = false;
+#pragma unroll
+                for (int i = 0; i < 6; ++i) {
+                    const bool used = i == 0 ? edge_l : (i == 5 ? edge_r : true);
+                    ahead = ahead || (used && static_cast<int>(tag_of(h[i]) - want) > 0);
+                }
+                if (ahead) {
+                    printf("sweep protocol violation: cta %d warp %d lane %d step %d want %u\n",
+                           static_cast<int>(blockIdx.x), wu * nwv + wv, lane, j, want);
+                    __trap();
+                }
+#endif
                 return ok;
             };
             long long spins = 0;
@@ -1066,7 +1087,13 @@ int width_class(int nwv) { return nwv <= 2 ? 2 : (nwv <= 4 ? 4 : 16); }
 }  // namespace
 extern int g_sweep_rw;  // sweep.cu
 namespace {
-int preferred_rw(int kind) { return g_sweep_rw >= 0 ? g_sweep_rw : (kind == kBlend ? 1 : 0); }
+// Blend runs one row per warp (16 warps) in both arithmetic modes: its f64
+// replica spills a little at 96 registers there, yet the spill-free 2x2 shape
+// measured slower (512^3 lambda = 0.5 exact: 193 vs 154 ms, profiles/r02_variants.txt).
+int preferred_rw(int kind, bool f64 = false) {
+    (void)f64;
+    return g_sweep_rw >= 0 ? g_sweep_rw : (kind == kBlend ? 1 : 0);
+}
 // The preferred shape exists for (R, width class, tb)?
 bool rw_pref_exists(int R, int mw, bool tb, int rw) {
 #define GD_CASE(RWW, NW, MM, NS, T, C) \
@@ -1092,7 +1119,7 @@ template <int KIND, bool F64>
 cudaError_t dispatch_r(int R, bool tb, const CUtensorMap& tm_d, const CUtensorMap& tm_i,
                        const SweepParams& p, cudaStream_t s) {
     const int mw = width_class(p.nwv);
-    RwSel sel(R, mw, tb, preferred_rw(KIND));
+    RwSel sel(R, mw, tb, preferred_rw(KIND, F64));
     const bool cl = p.cs > 1;
 #define GD_CASE(RWW, NW, MM, NS, T, C)                               \
     if (R == RWW * NW && mw == MM && tb == T && cl == C && sel.ok(RWW)) \
@@ -1105,7 +1132,7 @@ cudaError_t dispatch_r(int R, bool tb, const CUtensorMap& tm_d, const CUtensorMa
 template <int KIND, bool F64>
 int dispatch_cores(int R, bool tb, int nwv, int cs) {
     const int mw = width_class(nwv);
-    RwSel sel(R, mw, tb, preferred_rw(KIND));
+    RwSel sel(R, mw, tb, preferred_rw(KIND, F64));
 #define GD_CASE(RWW, NW, MM, NS, T, C)                                      \
     if (R == RWW * NW && mw == MM && tb == T && (cs > 1) == C && sel.ok(RWW))  \
         return C ? coresident_clusters<KIND, F64, RWW, NW, NS, MM, T, C>(nwv, cs) \

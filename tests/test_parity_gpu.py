@@ -329,10 +329,10 @@ def test_cuda_matches_golden(gd, path):
 
 @pytest.mark.parametrize("lam", LAMBDAS)
 def test_layout_planner_batch(gd, oracle, lam):
-    """A batch of narrow volumes: the planner runs the z pass on [x][z][y] and
-    the y pass on [y][x][z] (rows along the short x axis: fewer strips, more
-    volumes per launch group), rotating the distance between layouts; every
-    volume stays bit-exact / within tolerance."""
+    """A batch of narrow volumes: the planner runs the z pass on [x][z][y] (rows
+    along the short x axis: 6 strips per volume instead of 12, one launch group
+    instead of two), rotating the distance between layouts; every volume stays
+    bit-exact / within tolerance."""
     rng = np.random.default_rng(43)
     B, shape = 64, (40, 48, 24)
     imgs = dyadic_image(rng, (B,) + shape)
@@ -344,7 +344,6 @@ def test_layout_planner_batch(gd, oracle, lam):
     g = gd.generalized_geodesic_batched(imgs, masks, sp, lam, 1e10, 2)
     log = [r for r in gd.launch_log(reset=True) if r["f64"] == 0]
     assert {r["layout"] for r in log if r["axis"] == 0} == {1}, log
-    assert {r["layout"] for r in log if r["axis"] == 1} == {2}, log
     for b in range(0, B, 9):
         _check(g[b], oracle.generalized_geodesic(imgs[b], masks[b], sp, lam, 1e10, 2), lam)
 
