@@ -324,6 +324,19 @@ __global__ void subtract_kernel(const float* a, const float* b, float* out, long
         out[i] = a[i] - b[i];
 }
 
+// Experiment only (gd_debug_background_copy): a float4 copy loop run on a few
+// CTAs with a large dynamic shared-memory request, so they can only occupy SMs
+// the persistent sweep leaves free -- background HBM traffic to measure how
+// much the sweep's halo latency suffers from it.
+__global__ void background_copy_kernel(const float4* src, float4* dst, long long n4, int reps) {
+    extern __shared__ float4 pad[];
+    if (threadIdx.x == 0 && n4 < 0) pad[0] = src[0];  // keep the allocation
+    for (int r = 0; r < reps; ++r)
+        for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n4;
+             i += static_cast<long long>(gridDim.x) * blockDim.x)
+            dst[i] = __ldcs(src + i);
+}
+
 __global__ void reset_check_kernel(ImageCheck* c) {
     *c = ImageCheck{-1000, 1000, 0, 0, 0, 0};
 }
@@ -494,6 +507,16 @@ cudaError_t launch_threshold_count(const VolView& v, const float* mask, float* o
                                    unsigned long long* n_complement, cudaStream_t s) {
     const long long n = v.count();
     threshold_count_kernel<<<grid_for(n, 256), 256, 0, s>>>(v, mask, out, n_complement, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_background_copy(const float* src, float* dst, long long n, int ctas,
+                                   int smem_bytes, int reps, cudaStream_t s) {
+    cudaFuncSetAttribute(background_copy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         smem_bytes);
+    background_copy_kernel<<<ctas, 512, smem_bytes, s>>>(reinterpret_cast<const float4*>(src),
+                                                          reinterpret_cast<float4*>(dst), n / 4,
+                                                          reps);
     return cudaGetLastError();
 }
 

@@ -50,6 +50,8 @@ cudaError_t launch_hard_seeds(const VolView& mv, const float* mask, const VolVie
 // out = [M >= 0.5] and the count of its complement (geodesic_erode prologue).
 cudaError_t launch_threshold_count(const VolView& v, const float* mask, float* out,
                                    unsigned long long* n_complement, cudaStream_t s);
+cudaError_t launch_background_copy(const float* src, float* dst, long long n, int ctas,
+                                   int smem_bytes, int reps, cudaStream_t s);
 cudaError_t launch_subtract(const float* a, const float* b, float* out, long long n,
                             cudaStream_t s);
 cudaError_t launch_max_change(const VolView& v, const float* before, const float* after,

@@ -9,6 +9,7 @@
 #include <string>
 
 #include "../../include/geodist_b200.h"
+#include "aux_kernels.cuh"
 #include "engine.cuh"
 
 namespace gdb {
@@ -420,6 +421,15 @@ int gd_fill_splitmix(float* device_out, long long n, unsigned long long seed, vo
 }
 
 }  // extern "C"
+
+// Experiment: background HBM copy traffic on `stream` from `ctas` CTAs that each
+// request `smem_bytes` of shared memory (placement on SMs the sweep leaves free).
+extern "C" int gd_debug_background_copy(const float* src, float* dst, long long n, int ctas,
+                                        int smem_bytes, int reps, void* stream) {
+    cudaError_t e = gdb::launch_background_copy(src, dst, n, ctas, smem_bytes, reps,
+                                                static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? GD_OK : cuda_fail(e, "background copy");
+}
 
 // Diagnostics: co-resident CTA capacity of one sweep configuration.
 extern "C" int gd_debug_coresident(int R, int nwv, int kind, int f64) {

@@ -429,7 +429,11 @@ Status run_sweep(StreamCtx& sc, const Work& w, int L, int axis, int first_orient
         std::getenv("GEODIST_SWEEP_CLUSTER") ? std::atoi(std::getenv("GEODIST_SWEEP_CLUSTER")) : -1;
     int cs = 1;
     // Spatial (lambda = 0) prefers pairs: 512^3 13.32 (cs 2) / 13.56 (cs 4) / 13.64 ms (L2 only).
-    const bool cs_default = (kind == kIntensity || kind == kSpatial) && nwv >= 4 && ntu >= 64;
+    static const bool blend_cl = !(std::getenv("GEODIST_BLEND_CLUSTER") &&
+                                   std::atoi(std::getenv("GEODIST_BLEND_CLUSTER")) == 0);
+    const bool cs_default =
+        (kind == kIntensity || kind == kSpatial || (kind == kBlend && blend_cl)) && nwv >= 4 &&
+        ntu >= 64;
     if (R && !tb && ntu > 1 && (cs_env >= 0 || cs_default) && sweep_has_cluster(R, nwv, kind)) {
         const long long ctas = static_cast<long long>(group) * ntu;
         const int first = cs_env >= 0 ? cs_env : (kind == kSpatial ? 2 : 4);

@@ -1075,7 +1075,8 @@ int coresident(int nwv) {
     X(1, 1, 4, 6, false, false) X(2, 1, 4, 6, false, false) X(2, 2, 4, GD_NST4, false, false) \
     X(2, 2, 4, GD_NST4, true, false) X(2, 2, 4, GD_NST4, false, true)                       \
     X(4, 2, 4, 6, false, false) X(1, 4, 4, 6, false, false)                                 \
-    X(1, 1, 16, 6, false, false) X(2, 1, 16, 6, false, false) X(4, 1, 16, 6, false, false)
+    X(1, 1, 16, 6, false, false) X(2, 1, 16, 6, false, false) X(4, 1, 16, 6, false, false)     \
+    X(1, 4, 2, 6, false, true) X(1, 4, 4, 6, false, true)
 
 int width_class(int nwv) { return nwv <= 2 ? 2 : (nwv <= 4 ? 4 : 16); }
 

@@ -23,8 +23,8 @@ timeout 900 python bench.py --config batch64 --steps 5 > $O/${T}_bench_batch.jso
 timeout 900 python tools/time_configs.py --reps 5 > $O/${T}_configs.txt 2>&1
 timeout 1800 python tools/parity_configs.py > $O/${T}_parity.jsonl 2> $O/${T}_parity.err
 timeout 900 python tools/batch_shards.py > $O/${T}_batch_shards.txt 2>&1
-timeout 300 python tools/prof_step.py --reps 1 > $O/${T}_plain.log 2>&1 && \
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+GEODIST_SWEEP_NOCOOP=1 timeout 300 python tools/prof_step.py --reps 1 > $O/${T}_plain.log 2>&1 && \
+GEODIST_SWEEP_NOCOOP=1 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file $O/${T}_launches.csv python tools/prof_step.py --reps 1 > $O/${T}_ncu_ll.log 2>&1
 python tools/launch_list.py $O/${T}_launches.csv "one generalized_geodesic transform, 512^3, spacing (1,1,2.5), lambda=1, it=4" "python tools/prof_step.py --reps 1" > $O/${T}_launches_summary.csv 2>&1
 GEODIST_SWEEP_NOCOOP=1 timeout 300 python tools/prof_step.py --reps 1 > $O/${T}_plain_nocoop.log 2>&1 && \
