@@ -4,6 +4,7 @@
 // stream.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -127,6 +128,113 @@ int run(int mem, void* stream, long long n, const float* img, const float* aux, 
     return GD_OK;
 }
 
+// Batched host-memory calls pipeline over chunks of volumes (volumes are
+// independent): chunk k's H2D on a copy-in stream, its transform on the compute
+// stream, its D2H on a copy-out stream, each ordered by events, with three
+// device staging slots -- so PCIe in, PCIe out (full duplex) and compute overlap.
+// The transforms are enqueued without host synchronisation (the device-side
+// gates), so the whole pipeline is issued up front.  On a deferred error the
+// caller's output may hold partial results (the single-volume path leaves it
+// untouched).
+struct Pipeline {
+    std::mutex mu;
+    cudaStream_t in = nullptr, comp = nullptr, out = nullptr;
+    void* p[3][3] = {};
+    size_t n[3] = {0, 0, 0};
+    cudaEvent_t ev_in[3] = {}, ev_comp[3] = {}, ev_out[3] = {};
+    bool ready = false;
+    bool init() {
+        if (ready) return true;
+        if (cudaStreamCreateWithFlags(&in, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&comp, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&out, cudaStreamNonBlocking) != cudaSuccess)
+            return false;
+        for (int k = 0; k < 3; ++k)
+            if (cudaEventCreateWithFlags(&ev_in[k], cudaEventDisableTiming) != cudaSuccess ||
+                cudaEventCreateWithFlags(&ev_comp[k], cudaEventDisableTiming) != cudaSuccess ||
+                cudaEventCreateWithFlags(&ev_out[k], cudaEventDisableTiming) != cudaSuccess)
+                return false;
+        ready = true;
+        return true;
+    }
+    bool ensure(int slot, size_t bytes) {
+        if (bytes <= n[slot]) return true;
+        for (int a = 0; a < 3; ++a) {
+            if (p[slot][a]) cudaFree(p[slot][a]);
+            p[slot][a] = nullptr;
+        }
+        n[slot] = 0;
+        for (int a = 0; a < 3; ++a)
+            if (cudaMalloc(&p[slot][a], bytes) != cudaSuccess) return false;
+        n[slot] = bytes;
+        return true;
+    }
+};
+
+Pipeline& pipeline() {
+    static Pipeline pl[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return pl[dev & 63];
+}
+
+// fn(img, mask, out, nvol, stream) transforms nvol volumes on device pointers.
+template <class F>
+int run_batched_host(long long vol_elems, int batch, const float* img, const float* mask,
+                     float* out, void* user_stream, F&& fn) {
+    if (int rc = check_device()) return rc;
+    Pipeline& pl = pipeline();
+    std::lock_guard<std::mutex> lk(pl.mu);
+    if (!pl.init()) return fail(GD_CUDA_ERROR, "pipeline streams");
+    // ~8 chunks of at least 64 MB per array: enough to overlap, few enough to
+    // keep launch groups full
+    const long long vol_bytes = vol_elems * static_cast<long long>(sizeof(float));
+    int per = std::max(1, (batch + 7) / 8);
+    while (per < batch && static_cast<long long>(per) * vol_bytes < (64ll << 20)) ++per;
+    const int chunks = (batch + per - 1) / per;
+    cudaError_t e;
+    cudaStream_t us = static_cast<cudaStream_t>(user_stream);
+    // the caller's stream ordering: start after its pending work
+    if ((e = cudaEventRecord(pl.ev_out[2], us)) != cudaSuccess) return cuda_fail(e, "event");
+    if ((e = cudaStreamWaitEvent(pl.in, pl.ev_out[2], 0)) != cudaSuccess) return cuda_fail(e, "wait");
+    for (int c = 0; c < chunks; ++c) {
+        const int slot = c % 3;
+        const int b0 = c * per, nv = std::min(per, batch - b0);
+        const size_t bytes = static_cast<size_t>(nv) * vol_bytes;
+        if (c >= 3) {  // the slot's previous chunk must have left it
+            if ((e = cudaStreamWaitEvent(pl.in, pl.ev_comp[slot], 0)) != cudaSuccess ||
+                (e = cudaStreamWaitEvent(pl.in, pl.ev_out[slot], 0)) != cudaSuccess)
+                return cuda_fail(e, "pipeline wait");
+        }
+        if (!pl.ensure(slot, static_cast<size_t>(per) * vol_bytes))
+            return fail(GD_CUDA_ERROR, "device allocation failed");
+        float* di = static_cast<float*>(pl.p[slot][0]);
+        float* dm = static_cast<float*>(pl.p[slot][1]);
+        float* dout = static_cast<float*>(pl.p[slot][2]);
+        const size_t off = static_cast<size_t>(b0) * vol_elems;
+        if ((e = cudaMemcpyAsync(di, img + off, bytes, cudaMemcpyHostToDevice, pl.in)) != cudaSuccess ||
+            (e = cudaMemcpyAsync(dm, mask + off, bytes, cudaMemcpyHostToDevice, pl.in)) != cudaSuccess ||
+            (e = cudaEventRecord(pl.ev_in[slot], pl.in)) != cudaSuccess ||
+            (e = cudaStreamWaitEvent(pl.comp, pl.ev_in[slot], 0)) != cudaSuccess)
+            return cuda_fail(e, "pipeline H2D");
+        gdb::Status st = fn(di, dm, dout, nv, pl.comp);
+        if (!st.ok()) {
+            cudaDeviceSynchronize();
+            return fail(st);
+        }
+        if ((e = cudaEventRecord(pl.ev_comp[slot], pl.comp)) != cudaSuccess ||
+            (e = cudaStreamWaitEvent(pl.out, pl.ev_comp[slot], 0)) != cudaSuccess ||
+            (e = cudaMemcpyAsync(out + off, dout, bytes, cudaMemcpyDeviceToHost, pl.out)) != cudaSuccess ||
+            (e = cudaEventRecord(pl.ev_out[slot], pl.out)) != cudaSuccess)
+            return cuda_fail(e, "pipeline D2H");
+    }
+    if ((e = cudaStreamSynchronize(pl.out)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(pl.comp)) != cudaSuccess)
+        return cuda_fail(e, "stream sync");
+    gdb::Status w = gdb::take_deferred();
+    return w.ok() ? GD_OK : fail(w);
+}
+
 int policy_of(const gd_policy* p, gdb::Policy* out) {
     *out = gdb::Policy{};
     if (!p || !p->to_fixpoint) return GD_OK;
@@ -161,18 +269,8 @@ int gd_generalized_geodesic_batched(const gd_grid* grid, int batch, const float*
                                     const float* soft_masks, double lambda, double nu,
                                     int iterations, float* out, int mem, void* stream,
                                     gd_stats* stats) {
-    gdb::GridDesc g;
-    if (int rc = grid_of(grid, &g)) return rc;
-    if (batch < 1) return fail(GD_INVALID_ARGUMENT, "batch must be >= 1");
-    if (!images || !soft_masks || !out) return fail(GD_INVALID_ARGUMENT, "null buffer");
-    gdb::ScanStats st;
-    int rc = run(mem, stream, g.voxels() * batch, images, soft_masks, out, false,
-                 [&](const float* i, const float* m, float* o, cudaStream_t s) {
-                     return gdb::generalized_geodesic(g, batch, i, m, o, lambda, nu, iterations,
-                                                      s, &st);
-                 });
-    fill_stats(stats, st);
-    return rc;
+    return gd_generalized_geodesic_ex(grid, batch, images, soft_masks, lambda, nu, iterations,
+                                      nullptr, out, mem, stream, stats);
 }
 
 int gd_generalized_geodesic_ex(const gd_grid* grid, int batch, const float* images,
@@ -186,11 +284,32 @@ int gd_generalized_geodesic_ex(const gd_grid* grid, int batch, const float* imag
     if (batch < 1) return fail(GD_INVALID_ARGUMENT, "batch must be >= 1");
     if (!images || !soft_masks || !out) return fail(GD_INVALID_ARGUMENT, "null buffer");
     gdb::ScanStats st;
-    int rc = run(mem, stream, g.voxels() * batch, images, soft_masks, out, false,
+    int rc;
+    if (mem == GD_MEM_HOST && batch >= 2 && !pol.fixpoint) {
+        // validate before anything is enqueued (the engine repeats it per chunk)
+        // (TransformParams::validate, grid.cpp:67-78)
+        if (!(lambda >= 0.0 && lambda <= 1.0))
+            return fail(GD_INVALID_ARGUMENT, "lambda must lie in [0, 1], got " + std::to_string(lambda));
+        if (!(nu >= 0.0)) return fail(GD_INVALID_ARGUMENT, "nu must be >= 0, got " + std::to_string(nu));
+        if (iterations < 1)
+            return fail(GD_INVALID_ARGUMENT, "iterations must be >= 1, got " + std::to_string(iterations));
+        rc = run_batched_host(g.voxels(), batch, images, soft_masks, out, stream,
+                              [&](const float* i, const float* m, float* o, int nv,
+                                  cudaStream_t s) {
+                                  gdb::ScanStats cs;
+                                  gdb::Status r = gdb::generalized_geodesic(
+                                      g, nv, i, m, o, lambda, nu, iterations, s, &cs, pol);
+                                  st.rounds = cs.rounds;
+                                  st.kernel_launches += cs.kernel_launches;
+                                  return r;
+                              });
+    } else {
+        rc = run(mem, stream, g.voxels() * batch, images, soft_masks, out, false,
                  [&](const float* i, const float* m, float* o, cudaStream_t s) {
                      return gdb::generalized_geodesic(g, batch, i, m, o, lambda, nu, iterations,
                                                       s, &st, pol);
                  });
+    }
     fill_stats(stats, st);
     return rc;
 }
