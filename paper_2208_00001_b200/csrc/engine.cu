@@ -463,6 +463,7 @@ Status run_sweep(StreamCtx& sc, const Work& w, int L, int axis, int first_orient
     p.cs = cs;
     p.lambda = lambda;
     p.lambda_f = static_cast<float>(lambda);
+    p.sqrt_lambda_f = static_cast<float>(std::sqrt(lambda));
     p.gate = gate;
     p.gate_mask = kGateMaskBad | kGateF64 | kGateSkip;
     p.gate_want = gate_want;
@@ -477,6 +478,7 @@ Status run_sweep(StreamCtx& sc, const Work& w, int L, int axis, int first_orient
             p.rho[k] = rho;
             p.c0[k] = blend_c0(lambda, rho);
             p.c0_f[k] = static_cast<float>(p.c0[k]);
+            p.c0l_f[k] = lambda > 0.0 ? static_cast<float>(p.c0[k] / lambda) : 0.0f;
         }
 
     // Single-row planes (2D images): the row-chain kernel, one CTA per image
@@ -668,7 +670,11 @@ Status move_dist(StreamCtx& sc, Work& w, int from, int to, bool need_img, cudaSt
 }
 
 // f64 arithmetic for blend (exact mode); lambda = 1 decides on the device.
-bool blend_f64(int kind) { return kind == kBlend && g_exact_blend.load(); }
+// The f32 blend form sqrt(lambda) * sqrt(di^2 + c0 / lambda) needs c0 / lambda
+// to stay far from f32 overflow: lambda below 1e-20 takes the f64 replica.
+bool blend_f64(int kind, double lambda) {
+    return kind == kBlend && (g_exact_blend.load() || lambda < 1e-20);
+}
 
 // --- layout planner ------------------------------------------------------------
 // Estimated device time (us) of one pass group on layout L: sequential plane
@@ -771,7 +777,7 @@ std::vector<int> plan_layouts(const Work& w, const std::vector<PassSpec>& passes
 Status run_passes(StreamCtx& sc, Work& w, const std::vector<PassSpec>& passes, double lambda,
                   const Gate& gate, cudaStream_t s, ScanStats* st) {
     const int kind = cost_kind(lambda);
-    const bool f64 = blend_f64(kind);
+    const bool f64 = blend_f64(kind, lambda);
     const bool img = kind != kSpatial;
     const std::vector<int> plan = plan_layouts(w, passes, kind, f64);
     int cur = kLC;

@@ -63,8 +63,11 @@ __device__ __forceinline__ float candidate(float pq, float iq, float ip, int k,
         } else {
             // MUFU.SQRT (about 1 ulp): the IEEE sqrtf adds a slow-path CALL per
             // candidate that serialises the 9-candidate min (3x slower step).
+            // sqrt(lambda di^2 + c0) as sqrt(lambda) * sqrt(di^2 + c0 / lambda):
+            // FADD, FFMA, MUFU.SQRT, FFMA per candidate instead of FADD, FMUL,
+            // FFMA, MUFU.SQRT, FADD (within the tolerance like the f32 form).
             const float di = ip - iq;
-            return pq + sqrt_approx(fmaf(p.lambda_f * di, di, p.c0_f[k]));
+            return fmaf(p.sqrt_lambda_f, sqrt_approx(fmaf(di, di, p.c0l_f[k])), pq);
         }
     }
 }

@@ -90,8 +90,10 @@ struct SweepParams {
     double rho[9];
     double c0[9];
     float c0_f[9];
+    float c0l_f[9];           // blend f32: c0 / lambda (cost = sqrt(lambda) * sqrt(di^2 + c0 / lambda))
     double lambda;
     float lambda_f;
+    float sqrt_lambda_f;
 };
 
 // Gate bits written by decide_kernel (aux_kernels.cu) for one transform.
