@@ -349,7 +349,8 @@ def main():
     import ctypes as C
     step_bytes = 3 * int(vox_rank) * 4
     streamed = step_bytes <= (2 << 30)
-    e2e_steps = args.e2e_steps or min(args.steps, 8 if streamed else 5)
+    # (8 steps = 12 GiB of pinned host memory per rank at 512^3; 4 when N > 1)
+    e2e_steps = args.e2e_steps or min(args.steps, (8 if world == 1 else 4) if streamed else 5)
     reps = e2e_steps if streamed else 1
     hfull = (reps * nv,) + tuple(shape)
     h_img = torch.empty(hfull, dtype=torch.float32, pin_memory=True)
