@@ -111,6 +111,24 @@ def test_batched_matches_per_volume(gd, oracle):
         assert bitwise_equal(g[b], r), b
 
 
+@pytest.mark.parametrize("shape,lam", [((1, 8), 1.0), ((3, 5), 0.0), ((2, 2, 2), 1.0),
+                                       ((2, 3, 4), 0.5)])
+def test_batch_beyond_grid_limit(gd, oracle, shape, lam):
+    """More volumes than one launch's 65535-CTA grid: the row-chain / plane-step
+    launches split the batch, the persistent kernel runs many launch groups."""
+    rng = np.random.default_rng(31)
+    B = 66000
+    imgs = dyadic_image(rng, (B,) + shape)
+    masks = np.ones((B,) + shape, np.float32)
+    flat = masks.reshape(B, -1)
+    flat[np.arange(B), rng.integers(0, flat.shape[1], B)] = 0.0
+    sp = (1.0,) * len(shape)
+    g = gd.generalized_geodesic_batched(imgs, masks, sp, lam, 1e10, 2)
+    for b in list(range(0, 20)) + list(range(65525, 65545)) + list(range(B - 20, B)):
+        r = oracle.generalized_geodesic(imgs[b], masks[b], sp, lam, 1e10, 2)
+        _check(g[b], r, lam)
+
+
 @pytest.mark.parametrize("lam", LAMBDAS)
 @pytest.mark.parametrize("shape", [(10, 70, 150), (6, 24, 100)])
 def test_batched_tall_strips(gd, oracle, lam, shape):
