@@ -1080,20 +1080,21 @@ int coresident(int nwv) {
 
 int width_class(int nwv) { return nwv <= 2 ? 2 : (nwv <= 4 ? 4 : 16); }
 
-// Rows-per-warp preference among shapes with the same R.  Blend runs R = 4 as
-// four warp rows of one row (16 consumer warps: its MUFU-heavy candidates need
-// the extra warps to hide latency; 23.1 vs 35.9 ms per 512^3 transform), the
-// min-plus kinds as two warp rows of two (fewer window builds per voxel; 13.3
-// vs 14.2 ms at lambda = 1).  -1: per-kind default; 0: the first listed.
+// Rows-per-warp preference among shapes with the same R.  The f64 blend replica
+// runs R = 4 as four warp rows of one row (16 consumer warps to hide its f64
+// latency; 128^3: 14.3 vs 25.3 ms), everything else -- f32 blend included, since
+// its candidate became sqrt(lambda) * sqrt(di^2 + c0/lambda) -- as two warp rows
+// of two (fewer window builds per voxel; lambda = 1: 13.3 vs 14.2 ms; f32 blend
+// 512^3: 15.2 vs 15.7 ms of sweep, 16 x 256x256x160: 21.5 vs 31.2 ms;
+// profiles/r02_variants.txt).  -1: per-kind default; 0: the first listed.
 }  // namespace
 extern int g_sweep_rw;  // sweep.cu
 namespace {
-// Blend runs one row per warp (16 warps) in both arithmetic modes: its f64
-// replica spills a little at 96 registers there, yet the spill-free 2x2 shape
-// measured slower (512^3 lambda = 0.5 exact: 193 vs 154 ms, profiles/r02_variants.txt).
+// The f64 blend replica runs one row per warp (16 warps): it spills a little at
+// 96 registers there, yet the spill-free 2x2 shape measured slower (512^3
+// lambda = 0.5 exact: 193 vs 154 ms, profiles/r02_variants.txt).
 int preferred_rw(int kind, bool f64 = false) {
-    (void)f64;
-    return g_sweep_rw >= 0 ? g_sweep_rw : (kind == kBlend ? 1 : 0);
+    return g_sweep_rw >= 0 ? g_sweep_rw : (kind == kBlend && f64 ? 1 : 0);
 }
 // The preferred shape exists for (R, width class, tb)?
 bool rw_pref_exists(int R, int mw, bool tb, int rw) {

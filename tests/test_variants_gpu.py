@@ -29,7 +29,7 @@ VARIANTS = {
     "cluster4": ({"GEODIST_SWEEP_CLUSTER": "4"},
                  "any:cs=4,nwv=1;any:cs=4,nwv=3,kind=1;any:cs=4,kind=0"),
     "cluster8": ({"GEODIST_SWEEP_CLUSTER": "8"}, "any:cs=8,nwv=1;any:cs=8,nwv=3"),
-    # the one-row-per-warp (16-warp) shape in clusters of 4: blend's default shape
+    # the one-row-per-warp (16-warp) shape in clusters of 4: the exact-blend (f64) shape
     "cluster4_rw1": ({"GEODIST_SWEEP_CLUSTER": "4", "GEODIST_SWEEP_RW": "1"},
                      "any:cs=4,rows=4,nwu=4;any:cs=4,nwu=4,kind=2"),
     "no_row_chain": ({"GEODIST_ROWCHAIN": "0"}, "any:path=0,rows=1;none:path=1"),

@@ -36,6 +36,13 @@ CONFIGS = {
     "probe_b4_256x256x160": dict(shape=(256, 256, 160), batch=4, lam=1.0, it=4, sp=(1.0, 1.0, 1.0)),
     "probe_b4_256x256x256": dict(shape=(256, 256, 256), batch=4, lam=1.0, it=4, sp=(1.0, 1.0, 1.0)),
 }
+# blend (0 < lambda < 1) probes of the strip shape choice
+CONFIGS["blend_128"] = dict(shape=(128, 128, 128), batch=0, lam=0.5, it=4, sp=(1.0, 1.0, 1.0))
+CONFIGS["blend_256"] = dict(shape=(256, 256, 256), batch=0, lam=0.5, it=4, sp=(1.0, 1.0, 1.0))
+CONFIGS["blend_b16_256x256x160"] = dict(shape=(256, 256, 160), batch=16, lam=0.5, it=4,
+                                        sp=(1.0, 1.0, 1.0))
+CONFIGS["blend_1024x1024x64"] = dict(shape=(64, 1024, 1024), batch=0, lam=0.5, it=2,
+                                     sp=(1.0, 1.0, 1.0))
 for _w in (132, 160, 192, 224, 252, 255):
     CONFIGS[f"probeW_{_w}"] = dict(shape=(256, 256, _w), batch=0, lam=1.0, it=1, sp=(1.0, 1.0, 1.0))
 CONFIGS["probeW_160_l0"] = dict(shape=(256, 256, 160), batch=0, lam=0.0, it=1, sp=(1.0, 1.0, 1.0))
