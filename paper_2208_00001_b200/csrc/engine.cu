@@ -429,8 +429,9 @@ Status run_sweep(StreamCtx& sc, const Work& w, int L, int axis, int first_orient
         std::getenv("GEODIST_SWEEP_CLUSTER") ? std::atoi(std::getenv("GEODIST_SWEEP_CLUSTER")) : -1;
     int cs = 1;
     // Spatial (lambda = 0) prefers pairs: 512^3 13.32 (cs 2) / 13.56 (cs 4) / 13.64 ms (L2 only).
-    // Blend's 16-warp shape measured slower clustered (512^3 lambda = 0.5: 21.3 ms
-    // in clusters of 4, 20.6 of 2, 17.7 L2-only; profiles/r02_variants.txt):
+    // Blend measured slower clustered in both its shapes (512^3 lambda = 0.5, sweep:
+    // two rows per warp 19.4 ms in clusters of 4, 18.4 of 2, 15.2 L2-only; one row
+    // per warp 21.3 / 20.6 / 17.7 total; profiles/r02_variants.txt):
     // opt-in only (GEODIST_BLEND_CLUSTER=1).
     static const bool blend_cl = std::getenv("GEODIST_BLEND_CLUSTER") &&
                                  std::atoi(std::getenv("GEODIST_BLEND_CLUSTER")) == 1;
