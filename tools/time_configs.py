@@ -36,6 +36,10 @@ CONFIGS = {
     "probe_b4_256x256x160": dict(shape=(256, 256, 160), batch=4, lam=1.0, it=4, sp=(1.0, 1.0, 1.0)),
     "probe_b4_256x256x256": dict(shape=(256, 256, 256), batch=4, lam=1.0, it=4, sp=(1.0, 1.0, 1.0)),
 }
+# 2D row-chain probes
+CONFIGS["2d_512_b64"] = dict(shape=(512, 512), batch=64, lam=1.0, it=2, sp=(1.0, 1.0))
+CONFIGS["2d_256_l05"] = dict(shape=(256, 256), batch=0, lam=0.5, it=2, sp=(1.0, 1.0))
+CONFIGS["2d_1024"] = dict(shape=(1024, 1024), batch=0, lam=1.0, it=2, sp=(1.0, 1.0))
 # blend (0 < lambda < 1) probes of the strip shape choice
 CONFIGS["blend_128"] = dict(shape=(128, 128, 128), batch=0, lam=0.5, it=4, sp=(1.0, 1.0, 1.0))
 CONFIGS["blend_256"] = dict(shape=(256, 256, 256), batch=0, lam=0.5, it=4, sp=(1.0, 1.0, 1.0))
