@@ -352,10 +352,19 @@ def main():
     # (8 steps = 12 GiB of pinned host memory per rank at 512^3; 4 when N > 1)
     e2e_steps = args.e2e_steps or min(args.steps, (8 if world == 1 else 4) if streamed else 5)
     reps = e2e_steps if streamed else 1
-    hfull = (reps * nv,) + tuple(shape)
-    h_img = torch.empty(hfull, dtype=torch.float32, pin_memory=True)
-    h_mask = torch.empty(hfull, dtype=torch.float32, pin_memory=True)
-    h_out = torch.empty(hfull, dtype=torch.float32, pin_memory=True)
+    while True:  # fewer streamed steps if the host cannot pin that much memory
+        hfull = (reps * nv,) + tuple(shape)
+        try:
+            h_img = torch.empty(hfull, dtype=torch.float32, pin_memory=True)
+            h_mask = torch.empty(hfull, dtype=torch.float32, pin_memory=True)
+            h_out = torch.empty(hfull, dtype=torch.float32, pin_memory=True)
+            break
+        except RuntimeError:
+            h_img = h_mask = h_out = None
+            if reps <= 2:
+                raise
+            reps //= 2
+            e2e_steps = reps
     img_c, mask_c = img.reshape((nv,) + tuple(shape)).cpu(), mask.reshape((nv,) + tuple(shape)).cpu()
     for r in range(reps):
         h_img[r * nv:(r + 1) * nv].copy_(img_c)
