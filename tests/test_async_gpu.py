@@ -126,3 +126,38 @@ def test_batched_host_pipeline(gd, oracle):
         gd.generalized_geodesic_batched(imgs, masks, (1.0, 1.0, 2.5), 1.0, 1e10, 2)
     masks[11, 0, 0, 0] = 1.0
     gd.generalized_geodesic_batched(imgs, masks, (1.0, 1.0, 2.5), 1.0, 1e10, 2)
+
+
+def test_concurrent_streams_are_independent(gd, torch_cuda):
+    """Transforms enqueued on several CUDA streams at once (each stream has its own
+    workspace, halo words and gate) give exactly the single-stream results."""
+    torch = torch_cuda
+    shape, B, ns = (24, 40, 96), 12, 3
+    img = torch.empty((B,) + shape, device="cuda")
+    for b in range(B):
+        gd.device.fill_splitmix(img[b], 300 + b)
+    mask = torch.ones_like(img)
+    mask[:, 12, 20, 48] = 0.0
+    want = {}
+    for lam in (0.0, 0.6, 1.0):
+        ref = torch.empty_like(img)
+        gd.device.generalized_geodesic(img, mask, ref, (1.0, 1.0, 2.5), lam, 1e10, 3, batch=B)
+        want[lam] = ref
+    torch.cuda.synchronize()
+    cur = torch.cuda.current_stream()
+    streams = [torch.cuda.Stream() for _ in range(ns)]
+    outs = {lam: torch.full_like(img, -1.0) for lam in want}
+    per = B // ns
+    for lam in want:  # every stream busy with every lambda, interleaved
+        for i, s in enumerate(streams):
+            s.wait_stream(cur)
+            with torch.cuda.stream(s):
+                sl = slice(i * per, (i + 1) * per)
+                gd.device.generalized_geodesic(img[sl], mask[sl], outs[lam][sl], (1.0, 1.0, 2.5),
+                                               lam, 1e10, 3, batch=per, stream=s.cuda_stream)
+    for s in streams:
+        cur.wait_stream(s)
+    torch.cuda.synchronize()
+    gd.device.synchronize()
+    for lam in want:
+        assert torch.equal(outs[lam].view(torch.int32), want[lam].view(torch.int32)), lam
